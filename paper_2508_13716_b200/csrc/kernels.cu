@@ -1,0 +1,478 @@
+// sm_100a kernels for the halo-exchange + aggregation hot path.
+//
+//   K1/K2 cg_spmm        fused cache-lookup + gather CSR SpMM (fwd and bwd)
+//   K3    cg_copy_rows   halo staging / cache write-through over a pointer
+//                        table (local HBM, NVLink peers, mapped host tier)
+//   K6    cg_plan_frozen per-epoch JACA/FIFO plan after membership freezes
+//   K8    cg_softmax_ce  mean cross-entropy + logits gradient
+//   plus deterministic column sums, Adam and the synthetic-input hashes.
+//
+// All reductions are fixed-order (no float atomics): reruns are bitwise
+// identical.  See DESIGN.md for layouts and rooflines.
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/capgnn.h"
+
+extern void cg_set_error(const std::string &msg);
+extern int cg_cuda_fail(cudaError_t e, const char *what);
+
+#define CG_CHECK_LAUNCH(name)                                   \
+    do {                                                        \
+        cudaError_t _e = cudaGetLastError();                    \
+        if (_e != cudaSuccess) return cg_cuda_fail(_e, name);   \
+    } while (0)
+
+namespace {
+
+constexpr int kWarp = 32;
+
+__device__ __forceinline__ uint32_t mix32(uint32_t seed, uint32_t a, uint32_t b) {
+    uint32_t h = seed * 0x9E3779B1u + a * 0x85EBCA77u + b * 0xC2B2AE3Du;
+    h ^= h >> 16;
+    h *= 0x7FEB352Du;
+    h ^= h >> 15;
+    h *= 0x846CA68Bu;
+    h ^= h >> 16;
+    return h;
+}
+
+__device__ __forceinline__ float uniform_pm1(uint32_t seed, uint32_t a, uint32_t b) {
+    float x = __uint2float_rn(mix32(seed, a, b) >> 8);
+    return __fsub_rn(__fmul_rn(x, 1.1920928955078125e-07f), 1.0f);  // x*2^-23 - 1, exact
+}
+
+__global__ void k_hash_features(float *__restrict__ out, int64_t ld,
+                                const int32_t *__restrict__ vertex, int64_t n, int F,
+                                uint32_t seed, const float *__restrict__ row_scale) {
+    int64_t total = n * (int64_t)F;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = i / F;
+        int k = (int)(i - r * F);
+        float x = uniform_pm1(seed, (uint32_t)vertex[r], (uint32_t)k);
+        if (row_scale) x = __fmul_rn(x, row_scale[r]);
+        out[r * ld + k] = x;
+    }
+}
+
+__global__ void k_hash_labels(int32_t *__restrict__ out, const int32_t *__restrict__ vertex,
+                              int64_t n, int C, uint32_t seed) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (int32_t)(mix32(seed, (uint32_t)vertex[i], 0u) % (uint32_t)C);
+}
+
+// ---------------------------------------------------------------- K3 ------
+
+// One warp (or G-lane group) per row; 16-byte vectors when everything is
+// 16-byte aligned, scalar otherwise.
+template <bool VEC>
+__global__ void k_copy_rows(int64_t n, int F, const int32_t *__restrict__ src_id,
+                            const int32_t *__restrict__ src_row,
+                            const int32_t *__restrict__ dst_row,
+                            const float *const *__restrict__ tab,
+                            const int64_t *__restrict__ tab_ld, float *__restrict__ dst,
+                            int64_t ld_dst) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / kWarp;
+    int64_t nwarps = (int64_t)gridDim.x * blockDim.x / kWarp;
+    for (int64_t i = warp; i < n; i += nwarps) {
+        int sid = src_id[i];
+        int drow = dst_row[i];
+        if (sid < 0 || drow < 0) continue;
+        const float *s = tab[sid] + (int64_t)src_row[i] * tab_ld[sid];
+        float *d = dst + (int64_t)drow * ld_dst;
+        if (VEC) {
+            const float4 *s4 = reinterpret_cast<const float4 *>(s);
+            float4 *d4 = reinterpret_cast<float4 *>(d);
+            for (int c = lane; c < (F >> 2); c += kWarp) d4[c] = s4[c];
+        } else {
+            for (int c = lane; c < F; c += kWarp) d[c] = s[c];
+        }
+    }
+}
+
+// ---------------------------------------------------------------- K1 ------
+
+// G lanes per row, NCH float4 chunks per lane (row width F <= 4*G*NCH).
+// Column indices are loaded G at a time (coalesced), the halo indirection
+// (cache lookup -> slab / staging / owner row) is resolved per lane, then
+// broadcast with shuffles; UNR row gathers are in flight per lane.  The
+// accumulation order is the CSR order.
+template <int G, int NCH>
+__global__ void __launch_bounds__(256)
+k_spmm(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
+       const int32_t *__restrict__ col, int64_t n_direct, const int32_t *__restrict__ halo_row,
+       const float *__restrict__ X, int64_t ldx, const float *__restrict__ scale,
+       const float *__restrict__ addend, int64_t ld_add, const float *__restrict__ mask,
+       int64_t ld_mask, float *__restrict__ out, int64_t ldo) {
+    constexpr int UNR = 4;
+    const int lane = threadIdx.x & (G - 1);
+    const unsigned gmask = (G == 32) ? 0xffffffffu
+                                     : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+    const int nchunk = F >> 2;
+    int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+    int64_t ngrp = (int64_t)gridDim.x * blockDim.x / G;
+    for (int64_t r = grp; r < n_rows; r += ngrp) {
+        float4 acc[NCH];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int64_t e0 = rowptr[r], e1 = rowptr[r + 1];
+        for (int64_t eb = e0; eb < e1; eb += G) {
+            const int cnt = (int)((e1 - eb) < (int64_t)G ? (e1 - eb) : (int64_t)G);
+            int64_t myrow = 0;
+            if (lane < cnt) {
+                int64_t c = col[eb + lane];
+                myrow = (c < n_direct || halo_row == nullptr) ? c : halo_row[c - n_direct];
+            }
+            int j = 0;
+            for (; j + UNR <= cnt; j += UNR) {
+                float4 v[UNR][NCH];
+#pragma unroll
+                for (int u = 0; u < UNR; ++u) {
+                    int64_t rr = __shfl_sync(gmask, myrow, j + u, G);
+                    const float4 *src = reinterpret_cast<const float4 *>(X + rr * ldx);
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c) {
+                        int ch = lane + c * G;
+                        v[u][c] = ch < nchunk ? __ldg(src + ch) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < UNR; ++u)
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c) {
+                        acc[c].x += v[u][c].x;
+                        acc[c].y += v[u][c].y;
+                        acc[c].z += v[u][c].z;
+                        acc[c].w += v[u][c].w;
+                    }
+            }
+            for (; j < cnt; ++j) {
+                int64_t rr = __shfl_sync(gmask, myrow, j, G);
+                const float4 *src = reinterpret_cast<const float4 *>(X + rr * ldx);
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) {
+                    int ch = lane + c * G;
+                    if (ch < nchunk) {
+                        float4 t = __ldg(src + ch);
+                        acc[c].x += t.x;
+                        acc[c].y += t.y;
+                        acc[c].z += t.z;
+                        acc[c].w += t.w;
+                    }
+                }
+            }
+        }
+        const float s = scale ? scale[r] : 1.0f;
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            int ch = lane + c * G;
+            if (ch >= nchunk) continue;
+            float4 o = make_float4(acc[c].x * s, acc[c].y * s, acc[c].z * s, acc[c].w * s);
+            if (addend) {
+                float4 a = reinterpret_cast<const float4 *>(addend + r * ld_add)[ch];
+                o.x += a.x; o.y += a.y; o.z += a.z; o.w += a.w;
+            }
+            if (mask) {
+                float4 m = reinterpret_cast<const float4 *>(mask + r * ld_mask)[ch];
+                o.x = m.x > 0.f ? o.x : 0.f;
+                o.y = m.y > 0.f ? o.y : 0.f;
+                o.z = m.z > 0.f ? o.z : 0.f;
+                o.w = m.w > 0.f ? o.w : 0.f;
+            }
+            reinterpret_cast<float4 *>(out + r * ldo)[ch] = o;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- K8 ------
+
+__global__ void k_softmax_ce(int64_t n, int C, const float *__restrict__ logits, int64_t ld,
+                             const int32_t *__restrict__ label, float inv_n,
+                             float *__restrict__ grad, int64_t ldg, float *__restrict__ row_loss) {
+    const int lane = threadIdx.x & 31;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
+    int64_t nw = (int64_t)gridDim.x * blockDim.x / 32;
+    for (int64_t r = warp; r < n; r += nw) {
+        const float *z = logits + r * ld;
+        float mx = -INFINITY;
+        for (int c = lane; c < C; c += 32) mx = fmaxf(mx, z[c]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        float se = 0.f;
+        for (int c = lane; c < C; c += 32) se += expf(z[c] - mx);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+        const float lse = logf(se);
+        const int y = label[r];
+        for (int c = lane; c < C; c += 32) {
+            float p = expf(z[c] - mx - lse);
+            grad[r * ldg + c] = (p - (c == y ? 1.f : 0.f)) * inv_n;
+        }
+        if (lane == 0) row_loss[r] = lse - (z[y] - mx);
+    }
+}
+
+// Deterministic sum of x[0..n) into *out (single block, fixed order).
+__global__ void k_sum_fixed(const float *__restrict__ x, int64_t n, float *__restrict__ out) {
+    __shared__ double sh[1024];
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += (double)x[i];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = (float)sh[0];
+}
+
+// Column sums over m in fixed chunks: ws[chunk][n], then fixed-order reduce.
+__global__ void k_colsum_partial(int64_t M, int N, const float *__restrict__ D, int64_t ldd,
+                                 int64_t chunk, float *__restrict__ ws) {
+    int n = blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t c = blockIdx.y;
+    if (n >= N) return;
+    int64_t m0 = c * chunk, m1 = min(M, m0 + chunk);
+    float s = 0.f;
+    for (int64_t m = m0; m < m1; ++m) s += D[m * ldd + n];
+    ws[c * N + n] = s;
+}
+
+__global__ void k_reduce_chunks(int64_t n_out, int64_t n_chunks, const float *__restrict__ ws,
+                                float *__restrict__ out, int accumulate) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n_out) return;
+    float s = 0.f;
+    for (int64_t c = 0; c < n_chunks; ++c) s += ws[c * n_out + i];
+    out[i] = accumulate ? out[i] + s : s;
+}
+
+__global__ void k_adam(int64_t n, float *__restrict__ p, const float *__restrict__ g,
+                       float *__restrict__ m, float *__restrict__ v, float lr, float b1,
+                       float b2, float eps, float c1, float c2) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float gi = g[i];
+        float mi = b1 * m[i] + (1.f - b1) * gi;
+        float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+        m[i] = mi;
+        v[i] = vi;
+        p[i] -= lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+    }
+}
+
+// ---------------------------------------------------------------- K6 ------
+
+__device__ __forceinline__ bool fresh(int32_t ver, int e, int s) { return s < 0 || e - ver <= s; }
+
+// One thread per halo-union vertex u.  Requesters are visited in the
+// reference's global lookup order (position in the requester's halo, then
+// partition slot), which is the only order that matters for u because,
+// with frozen membership, a lookup of u touches only u's own entries.
+__global__ void k_plan_frozen(cg_plan_static st, int e, int s, int me, int32_t *req_ver,
+                              int32_t *glob_ver, int32_t *halo_row, int32_t *stage_src,
+                              int32_t *stage_row, int32_t *stage_dst, int32_t *gw_slot,
+                              int64_t *counts, int32_t *flag, int32_t staging_base,
+                              int32_t n_devices, int8_t *outcome) {
+    int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (u >= st.n_union) return;
+    const int32_t g = st.gslot[u];
+    const int32_t odev = st.owner_dev[u], orow = st.owner_row[u];
+    bool gdirty = false;
+    for (int64_t k = st.req_off[u]; k < st.req_off[u + 1]; ++k) {
+        const int32_t slot = st.req_slot[k];
+        const int32_t part = st.req_part[k];
+        int oc, ver;
+        if (slot >= 0 && fresh(req_ver[k], e, s)) {
+            oc = 0;
+            ver = req_ver[k];
+        } else if (g >= 0 && fresh(glob_ver[g], e, s)) {
+            oc = 1;
+            ver = glob_ver[g];
+            if (slot >= 0) req_ver[k] = ver;
+        } else {
+            oc = 2;
+            ver = e;
+            // admit modes: 0 never (capacity 0), 1 always (room left, or FIFO
+            // evicts), 2 only if the score beats the resident minimum (JACA)
+            if (g >= 0) { glob_ver[g] = e; gdirty = true; }
+            else if (st.gfree == 1 || (st.gfree == 2 && st.score[u] > st.gmin)) *flag = 1;
+            if (slot >= 0) req_ver[k] = e;
+            else if (st.lfree[part] == 1 || (st.lfree[part] == 2 && st.score[u] > st.lmin[part]))
+                *flag = 1;
+        }
+        if (outcome) outcome[k] = (int8_t)oc;
+        atomicAdd(reinterpret_cast<unsigned long long *>(counts + 3 * part + oc), 1ull);
+        if (st.req_dev[k] != me) continue;
+        const int32_t pos = st.req_pos[k];
+        const bool cur = (ver < 1 ? 1 : ver) == e;
+        if (!st.req_needed[k]) {
+            halo_row[pos] = -1;
+            stage_src[pos] = -1;
+            continue;
+        }
+        if (oc == 0 && !cur) {  // stale local hit: read the slab in place
+            halo_row[pos] = slot;
+            stage_src[pos] = -1;
+            continue;
+        }
+        // value = owner's current row, or the global tier's snapshot
+        int src_id, src_row;
+        if (cur) { src_id = odev; src_row = orow; }
+        else { src_id = n_devices; src_row = g; }  // host tier (table entry n_devices)
+        if (slot >= 0) {  // write through into the local slab, read it there
+            stage_src[pos] = src_id;
+            stage_row[pos] = src_row;
+            stage_dst[pos] = slot;
+            halo_row[pos] = slot;
+        } else if (cur && odev == me) {  // co-resident owner: read in place
+            stage_src[pos] = -1;
+            halo_row[pos] = orow;
+        } else {
+            stage_src[pos] = src_id;
+            stage_row[pos] = src_row;
+            stage_dst[pos] = staging_base + pos;
+            halo_row[pos] = staging_base + pos;
+        }
+    }
+    if (g >= 0 && odev == me) {
+        // the owner materialises version-e content (and the warm entries at e=1)
+        bool need = gdirty || (e == 1 && glob_ver[g] <= 1);
+        gw_slot[u] = need ? g : -1;
+    }
+}
+
+inline int grid_for(int64_t work, int threads, int max_blocks = 148 * 16) {
+    int64_t b = (work + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > max_blocks) b = max_blocks;
+    return (int)b;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cg_hash_features(float *out, int64_t ld, const int32_t *vertex, int64_t n_rows, int F,
+                     uint32_t seed, const float *row_scale, void *stream) {
+    if (n_rows == 0) return 0;
+    k_hash_features<<<grid_for(n_rows * F, 256), 256, 0, (cudaStream_t)stream>>>(
+        out, ld, vertex, n_rows, F, seed, row_scale);
+    CG_CHECK_LAUNCH("k_hash_features");
+    return 0;
+}
+
+int cg_hash_labels(int32_t *out, const int32_t *vertex, int64_t n_rows, int C, uint32_t seed,
+                   void *stream) {
+    if (n_rows == 0) return 0;
+    k_hash_labels<<<grid_for(n_rows, 256), 256, 0, (cudaStream_t)stream>>>(out, vertex, n_rows,
+                                                                          C, seed);
+    CG_CHECK_LAUNCH("k_hash_labels");
+    return 0;
+}
+
+int cg_copy_rows(int64_t n, int F, const int32_t *src_id, const int32_t *src_row,
+                 const int32_t *dst_row, const float *const *tab, const int64_t *tab_ld,
+                 float *dst, int64_t ld_dst, void *stream) {
+    if (n == 0) return 0;
+    const int threads = 256;
+    int blocks = grid_for(n * 32, threads, 148 * 32);
+    bool vec = (F % 4 == 0) && (ld_dst % 4 == 0) && ((uintptr_t)dst % 16 == 0);
+    // source alignment is validated on the host side (tab_ld % 4 == 0, 16-B bases)
+    if (vec)
+        k_copy_rows<true><<<blocks, threads, 0, (cudaStream_t)stream>>>(
+            n, F, src_id, src_row, dst_row, tab, tab_ld, dst, ld_dst);
+    else
+        k_copy_rows<false><<<blocks, threads, 0, (cudaStream_t)stream>>>(
+            n, F, src_id, src_row, dst_row, tab, tab_ld, dst, ld_dst);
+    CG_CHECK_LAUNCH("k_copy_rows");
+    return 0;
+}
+
+int cg_spmm(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col, int64_t n_direct,
+            const int32_t *halo_row, const float *X, int64_t ldx, const float *scale,
+            const float *addend, int64_t ld_add, const float *mask, int64_t ld_mask, float *out,
+            int64_t ldo, void *stream) {
+    if (n_rows == 0) return 0;
+    if (F % 4 || ldx % 4 || ldo % 4 || (addend && ld_add % 4) || (mask && ld_mask % 4) ||
+        ((uintptr_t)X % 16) || ((uintptr_t)out % 16)) {
+        cg_set_error("cg_spmm: F and leading dims must be multiples of 4, buffers 16-B aligned");
+        return -1;
+    }
+    const int nchunk = F / 4;
+    const int threads = 256;
+    cudaStream_t st = (cudaStream_t)stream;
+#define CG_SPMM_LAUNCH(G, NCH)                                                              \
+    k_spmm<G, NCH><<<grid_for(n_rows * G, threads, 148 * 64), threads, 0, st>>>(           \
+        n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, scale, addend, ld_add, mask, \
+        ld_mask, out, ldo)
+    if (nchunk <= 8) CG_SPMM_LAUNCH(8, 1);
+    else if (nchunk <= 16) CG_SPMM_LAUNCH(16, 1);
+    else if (nchunk <= 32) CG_SPMM_LAUNCH(32, 1);
+    else if (nchunk <= 64) CG_SPMM_LAUNCH(32, 2);
+    else if (nchunk <= 96) CG_SPMM_LAUNCH(32, 3);
+    else if (nchunk <= 128) CG_SPMM_LAUNCH(32, 4);
+    else if (nchunk <= 160) CG_SPMM_LAUNCH(32, 5);
+    else {
+        cg_set_error("cg_spmm: F > 640 not supported");
+        return -1;
+    }
+#undef CG_SPMM_LAUNCH
+    CG_CHECK_LAUNCH("k_spmm");
+    return 0;
+}
+
+int cg_colsum(int64_t M, int N, const float *D, int64_t ldd, float *db, float *ws, void *stream) {
+    if (M == 0 || N == 0) return 0;
+    const int64_t chunk = 2048;
+    int64_t nch = (M + chunk - 1) / chunk;
+    dim3 grid((N + 127) / 128, (unsigned)nch);
+    cudaStream_t st = (cudaStream_t)stream;
+    k_colsum_partial<<<grid, 128, 0, st>>>(M, N, D, ldd, chunk, ws);
+    k_reduce_chunks<<<(N + 255) / 256, 256, 0, st>>>(N, nch, ws, db, 0);
+    CG_CHECK_LAUNCH("cg_colsum");
+    return 0;
+}
+
+int cg_softmax_ce(int64_t n_rows, int C, const float *logits, int64_t ld, const int32_t *label,
+                  float inv_n, float *grad, int64_t ldg, float *loss_out, float *ws,
+                  void *stream) {
+    if (n_rows == 0) return 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    k_softmax_ce<<<grid_for(n_rows * 32, 256, 148 * 32), 256, 0, st>>>(n_rows, C, logits, ld,
+                                                                      label, inv_n, grad, ldg, ws);
+    k_sum_fixed<<<1, 1024, 0, st>>>(ws, n_rows, loss_out);
+    CG_CHECK_LAUNCH("cg_softmax_ce");
+    return 0;
+}
+
+int cg_adam(int64_t n, float *param, const float *grad, float *m, float *v, float lr,
+            float beta1, float beta2, float eps, int step, void *stream) {
+    if (n == 0) return 0;
+    double c1 = 1.0 - pow((double)beta1, (double)step);
+    double c2 = 1.0 - pow((double)beta2, (double)step);
+    k_adam<<<grid_for(n, 256, 148 * 8), 256, 0, (cudaStream_t)stream>>>(
+        n, param, grad, m, v, lr, beta1, beta2, eps, (float)c1, (float)c2);
+    CG_CHECK_LAUNCH("k_adam");
+    return 0;
+}
+
+int cg_plan_frozen(const cg_plan_static *st, int epoch, int staleness, int me, int32_t *req_ver,
+                   int32_t *glob_ver, int32_t *halo_row, int32_t *stage_src, int32_t *stage_row,
+                   int32_t *stage_dst, int32_t *gw_slot, int64_t *counts, int32_t *flag,
+                   int32_t staging_base, int32_t n_devices, int8_t *outcome, void *stream) {
+    if (st->n_union == 0) return 0;
+    k_plan_frozen<<<(unsigned)((st->n_union + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        *st, epoch, staleness, me, req_ver, glob_ver, halo_row, stage_src, stage_row, stage_dst,
+        gw_slot, counts, flag, staging_base, n_devices, outcome);
+    CG_CHECK_LAUNCH("k_plan_frozen");
+    return 0;
+}
+
+}  // extern "C"
