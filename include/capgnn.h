@@ -3,8 +3,10 @@
  * CaPGNN's per-layer halo exchange + neighbour aggregation hot path.
  *
  * Conventions
- *   - every entry point returns int: 0 = OK, < 0 = error; cg_last_error()
- *     returns a thread-local message for the last failure on this thread;
+ *   - every entry point returns int: >= 0 = OK, < 0 = error; device entry
+ *     points return the number of kernels they launched (0 when there was
+ *     nothing to do); cg_last_error() returns a thread-local message for
+ *     the last failure on this thread;
  *   - plain pointers and sizes only; device buffers are owned by the caller
  *     (PyTorch caching allocator on the Python side) and only borrowed;
  *   - `stream` is a cudaStream_t passed as void*; nothing synchronises the
@@ -47,7 +49,7 @@ int cg_host_tier_unregister(void *host_ptr);
 /* Peer access and CUDA IPC for one-sided NVLink pulls between processes
  * (the reference models this as a cost only: devices.py:73-78).          */
 int cg_enable_peer_access(int device, int peer);
-int cg_ipc_get_handle(void *dev_ptr, uint8_t handle_out[64]);
+int cg_ipc_get_handle(void *dev_ptr, uint8_t handle_out[64], int64_t *offset);
 int cg_ipc_open_handle(const uint8_t handle[64], int device, void **dev_ptr);
 int cg_ipc_close_handle(void *dev_ptr);
 
@@ -57,6 +59,9 @@ int cg_hash_features(float *out, int64_t ld, const int32_t *vertex, int64_t n_ro
                      int F, uint32_t seed, const float *row_scale, void *stream);
 int cg_hash_labels(int32_t *out, const int32_t *vertex, int64_t n_rows, int C,
                    uint32_t seed, void *stream);
+/* X[r*ld + k] *= scale[r] (GCN source-degree pre-scaling of uploaded rows). */
+int cg_scale_rows(float *X, int64_t ld, int64_t n_rows, int F, const float *scale,
+                  void *stream);
 
 /* ---- K3: halo staging / cache write-through ---------------------------- */
 /* For i in [0, n): if src_id[i] >= 0 and dst_row[i] >= 0:

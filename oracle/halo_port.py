@@ -385,16 +385,19 @@ class PlanRun:
         return "\n".join(lines) + "\n"
 
 
-def plan_epochs(policy: str, caps, ranked, halo, score: dict, epochs: int,
-                staleness: int) -> PlanRun:
-    """simulator.run's lookup loop (simulator.py:185-226), round-robin."""
-    c_cpu, c_gpu = caps[0], caps[1]
-    cache = TwoLevel(policy, c_cpu, c_gpu, score if policy == "jaca" else score)
-    cache.warm(ranked)
-    run = PlanRun(cache=cache)
-    P = len(halo)
-    longest = max((len(h) for h in halo), default=0)
-    for e in range(1, epochs + 1):
+class Planner:
+    """Stepwise form of simulator.run's lookup loop (simulator.py:185-226)."""
+
+    def __init__(self, policy: str, caps, ranked, halo, score: dict):
+        self.cache = TwoLevel(policy, caps[0], caps[1], score)
+        self.cache.warm(ranked)
+        self.halo = halo
+        self.run = PlanRun(cache=self.cache)
+
+    def step(self, e: int, staleness: int) -> EpochPlan:
+        halo, cache = self.halo, self.cache
+        P = len(halo)
+        longest = max((len(h) for h in halo), default=0)
         oc = [np.empty(len(h), dtype=np.int8) for h in halo]
         vs = [np.empty(len(h), dtype=np.int64) for h in halo]
         before = cache.counts.copy()
@@ -404,9 +407,18 @@ def plan_epochs(policy: str, caps, ranked, halo, score: dict, epochs: int,
                     o, ver = cache.lookup(d, int(halo[d][r]), e, staleness)
                     oc[d][r] = o
                     vs[d][r] = ver
-        run.plans.append(EpochPlan(epoch=e, outcome=oc, version=vs,
-                                   counts=cache.counts - before))
-    return run
+        plan = EpochPlan(epoch=e, outcome=oc, version=vs, counts=cache.counts - before)
+        self.run.plans.append(plan)
+        return plan
+
+
+def plan_epochs(policy: str, caps, ranked, halo, score: dict, epochs: int,
+                staleness: int) -> PlanRun:
+    """All epochs of simulator.run's lookup loop, round-robin order."""
+    pl = Planner(policy, caps, ranked, halo, score)
+    for e in range(1, epochs + 1):
+        pl.step(e, staleness)
+    return pl.run
 
 
 # ---------------------------------------------------------------------------

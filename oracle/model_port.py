@@ -184,35 +184,36 @@ def _layer_params(spec, params, l):
     return params[2 * l:2 * l + 2] if spec.kind == "gcn" else params[3 * l:3 * l + 3]
 
 
-def partitioned_epochs(g, inner, halo, versions, spec: ModelSpec, X, y,
-                       params=None, epochs: int | None = None):
-    """Train for len(versions) epochs.
+class Trainer:
+    """Stepwise partitioned training (one call of ``step`` = one epoch)."""
 
-    versions[e-1][p] is the int array of served versions for partition p's
-    halo (ascending id), as produced by the cache plan (halo_port.plan_epochs
-    or the product planner).  Returns per-epoch (loss, logits) and params.
-    """
-    L = len(spec.dims) - 1
-    n = g.n
-    P = len(inner)
-    params = [p.astype(np.float64) for p in (params or init_params(spec.kind, spec.dims))]
-    opt = Adam(params, spec.lr)
-    norms = degree_norms(g) if spec.kind == "gcn" else None
-    ops = [local_operator(g, inner[p], halo[p], spec.kind, norms) for p in range(P)]
-    history: dict[int, list[np.ndarray]] = {}
-    outs = []
-    epochs = len(versions) if epochs is None else epochs
-    X = X.astype(np.float64)
-    for e in range(1, epochs + 1):
-        cur = [X]
-        used = []  # per layer, per partition: (H_in, agg)
+    def __init__(self, g, inner, halo, spec: ModelSpec, X, y, params=None):
+        self.g, self.inner, self.halo, self.spec = g, inner, halo, spec
+        self.L = len(spec.dims) - 1
+        self.P = len(inner)
+        self.params = [p.astype(np.float64) for p in (params or init_params(spec.kind, spec.dims))]
+        self.opt = Adam(self.params, spec.lr)
+        norms = degree_norms(g) if spec.kind == "gcn" else None
+        self.ops = [local_operator(g, inner[p], halo[p], spec.kind, norms) for p in range(self.P)]
+        self.history: dict[int, list[np.ndarray]] = {}
+        self.X = X.astype(np.float64)
+        self.y = y
+        self.e = 0
+
+    def step(self, versions_e) -> EpochOut:
+        """versions_e[p]: served versions of partition p's halo (ascending id)."""
+        spec, params, L, P, n = self.spec, self.params, self.L, self.P, self.g.n
+        inner, halo, ops, history = self.inner, self.halo, self.ops, self.history
+        self.e += 1
+        e = self.e
+        cur = [self.X]
+        used = []  # per layer: (per partition (H_in, agg), pre-activation)
         for l in range(L):
             H = cur[l]
             nxt = np.zeros((n, spec.dims[l + 1]))
             lay = []
             for p in range(P):
-                ver = versions[e - 1][p]
-                src = np.maximum(ver, 1)
+                src = np.maximum(versions_e[p], 1)
                 hal = H[halo[p]].copy()
                 for old in np.unique(src[src != e]):
                     sel = src == old
@@ -226,15 +227,15 @@ def partitioned_epochs(g, inner, halo, versions, spec: ModelSpec, X, y,
                     Y = H[inner[p]] @ lp[0] + agg @ lp[1] + lp[2]
                 nxt[inner[p]] = Y
                 lay.append((Hin, agg))
-            used.append((lay, nxt))  # nxt = pre-activation, for the ReLU mask
+            used.append((lay, nxt))
             cur.append(relu(nxt) if l < L - 1 else nxt)
         history[e] = cur
         logits = cur[L]
-        loss_sum, dY = softmax_ce(logits, y, n)
-        outs.append(EpochOut(epoch=e, loss=loss_sum / n, logits=logits.copy()))
+        loss_sum, dY = softmax_ce(logits, self.y, n)
+        out = EpochOut(epoch=e, loss=loss_sum / n, logits=logits.copy())
         grads = [np.zeros_like(p) for p in params]
         for l in range(L - 1, -1, -1):
-            lay, Ypre = used[l]
+            lay, _ = used[l]
             dH = np.zeros((n, spec.dims[l])) if l > 0 else None
             gi = 2 * l if spec.kind == "gcn" else 3 * l
             lp = _layer_params(spec, params, l)
@@ -260,8 +261,21 @@ def partitioned_epochs(g, inner, halo, versions, spec: ModelSpec, X, y,
                         np.add.at(dH, halo[p], dHin[n_in:])
             if l > 0:
                 dY = dH * (used[l - 1][1] > 0)
-        opt.step(params, grads)
-    return outs, params
+        self.opt.step(params, grads)
+        return out
+
+
+def partitioned_epochs(g, inner, halo, versions, spec: ModelSpec, X, y,
+                       params=None, epochs: int | None = None):
+    """Train for len(versions) epochs; returns per-epoch (loss, logits), params.
+
+    versions[e-1][p] is the int array of served versions for partition p's
+    halo (ascending id), as produced by the cache plan.
+    """
+    tr = Trainer(g, inner, halo, spec, X, y, params)
+    epochs = len(versions) if epochs is None else epochs
+    outs = [tr.step(versions[e]) for e in range(epochs)]
+    return outs, tr.params
 
 
 def full_graph_epochs(g, spec: ModelSpec, X, y, epochs: int, params=None):

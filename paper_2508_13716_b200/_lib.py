@@ -41,11 +41,12 @@ SIGNATURES = {
     "cg_host_tier_register": [P, SZ],
     "cg_host_tier_unregister": [P],
     "cg_enable_peer_access": [INT, INT],
-    "cg_ipc_get_handle": [P, P],
+    "cg_ipc_get_handle": [P, P, P],
     "cg_ipc_open_handle": [P, INT, P],
     "cg_ipc_close_handle": [P],
     "cg_hash_features": [P, I64, P, I64, INT, U32, P, P],
     "cg_hash_labels": [P, P, I64, INT, U32, P],
+    "cg_scale_rows": [P, I64, I64, INT, P, P],
     "cg_copy_rows": [I64, INT, P, P, P, P, P, P, I64, P],
     "cg_spmm": [I64, INT, P, P, I64, P, P, I64, P, P, I64, P, I64, P, I64, P],
     "cg_gemm": [I64, INT, INT, P, I64, P, INT, P, I64, P, INT, P, INT, P, P, I64, INT, P],
@@ -106,6 +107,14 @@ def lib():
     return _lib
 
 
+# device entry points report how many kernels they launched; the running
+# total is the bench's "gpu_launches" evidence
+KERNEL_ENTRY = {"cg_hash_features", "cg_hash_labels", "cg_scale_rows", "cg_copy_rows",
+                "cg_spmm", "cg_gemm", "cg_wgrad", "cg_colsum", "cg_softmax_ce", "cg_adam",
+                "cg_plan_frozen"}
+launches = {"total": 0}
+
+
 def call(name: str, *args) -> int:
     """Invoke an entry point; raise CapgnnError on a negative status."""
     rc = getattr(lib(), name)(*args)
@@ -114,6 +123,9 @@ def call(name: str, *args) -> int:
     if rc < 0:
         msg = lib().cg_last_error()
         raise CapgnnError(f"{name}: {msg.decode() if msg else 'error'}")
+    if name in KERNEL_ENTRY:
+        launches["total"] += rc
+        launches[name] = launches.get(name, 0) + rc
     return rc
 
 

@@ -1,5 +1,6 @@
 // Library plumbing for libcapgnn.so: error reporting, host tier, peers, IPC.
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -74,12 +75,31 @@ int cg_enable_peer_access(int device, int peer) {
     return e == cudaSuccess ? 0 : cg_cuda_fail(e, "cudaDeviceEnablePeerAccess");
 }
 
-int cg_ipc_get_handle(void *dev_ptr, uint8_t handle_out[64]) {
+int cg_ipc_get_handle(void *dev_ptr, uint8_t handle_out[64], int64_t *offset) {
+    // IPC handles name whole allocations; report where dev_ptr sits inside
+    // its allocation so the importer can rebase (the caching allocator
+    // sub-allocates tensors from larger segments).
+    // resolved through the runtime so the library never links libcuda
+    // directly (it must load on hosts without a driver for the CPU tests)
+    typedef CUresult (*range_fn)(CUdeviceptr *, size_t *, CUdeviceptr);
+    static range_fn get_range = nullptr;
+    if (!get_range) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        cudaError_t e0 = cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q);
+        if (e0 != cudaSuccess || !fn) return cg_cuda_fail(e0, "cudaGetDriverEntryPoint");
+        get_range = (range_fn)fn;
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    CUresult r = get_range(&base, &size, (CUdeviceptr)dev_ptr);
+    if (r != CUDA_SUCCESS) { cg_set_error("cuMemGetAddressRange failed"); return -1; }
     cudaIpcMemHandle_t h;
-    cudaError_t e = cudaIpcGetMemHandle(&h, dev_ptr);
+    cudaError_t e = cudaIpcGetMemHandle(&h, (void *)base);
     if (e != cudaSuccess) return cg_cuda_fail(e, "cudaIpcGetMemHandle");
     static_assert(sizeof(h) == 64, "ipc handle size");
     std::memcpy(handle_out, &h, 64);
+    *offset = (int64_t)((CUdeviceptr)dev_ptr - base);
     return 0;
 }
 

@@ -180,7 +180,7 @@ int cg_gemm(int64_t M, int N, int K1, const float *A1, int64_t lda1, const float
     k_gemm<<<grid, NT, 0, (cudaStream_t)stream>>>(M, N, K1, A1, lda1, B1, K2, A2, lda2, B2,
                                                  trans_b, bias, relu, row_scale, C, ldc);
     cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? 0 : cg_cuda_fail(e, "k_gemm");
+    return e == cudaSuccess ? 1 : cg_cuda_fail(e, "k_gemm");
 }
 
 int64_t cg_wgrad_workspace(int64_t M, int K, int N) {
@@ -201,7 +201,7 @@ int cg_wgrad(int64_t M, int K, int N, const float *A, int64_t lda, const float *
     int64_t n_out = (int64_t)K * N;
     k_wgrad_reduce<<<(unsigned)((n_out + 255) / 256), 256, 0, st>>>(n_out, nch, ws, dW);
     cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? 0 : cg_cuda_fail(e, "cg_wgrad");
+    return e == cudaSuccess ? 2 : cg_cuda_fail(e, "cg_wgrad");
 }
 
 }  // extern "C"

@@ -253,6 +253,16 @@ __global__ void k_reduce_chunks(int64_t n_out, int64_t n_chunks, const float *__
     out[i] = accumulate ? out[i] + s : s;
 }
 
+__global__ void k_scale_rows(float *__restrict__ X, int64_t ld, int64_t n, int F,
+                             const float *__restrict__ scale) {
+    int64_t total = n * (int64_t)F;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = i / F;
+        X[r * ld + (i - r * F)] *= scale[r];
+    }
+}
+
 __global__ void k_adam(int64_t n, float *__restrict__ p, const float *__restrict__ g,
                        float *__restrict__ m, float *__restrict__ v, float lr, float b1,
                        float b2, float eps, float c1, float c2) {
@@ -341,9 +351,9 @@ __global__ void k_plan_frozen(cg_plan_static st, int e, int s, int me, int32_t *
             halo_row[pos] = staging_base + pos;
         }
     }
-    if (g >= 0 && odev == me) {
+    if (odev == me) {
         // the owner materialises version-e content (and the warm entries at e=1)
-        bool need = gdirty || (e == 1 && glob_ver[g] <= 1);
+        bool need = g >= 0 && (gdirty || (e == 1 && glob_ver[g] <= 1));
         gw_slot[u] = need ? g : -1;
     }
 }
@@ -365,7 +375,7 @@ int cg_hash_features(float *out, int64_t ld, const int32_t *vertex, int64_t n_ro
     k_hash_features<<<grid_for(n_rows * F, 256), 256, 0, (cudaStream_t)stream>>>(
         out, ld, vertex, n_rows, F, seed, row_scale);
     CG_CHECK_LAUNCH("k_hash_features");
-    return 0;
+    return 1;
 }
 
 int cg_hash_labels(int32_t *out, const int32_t *vertex, int64_t n_rows, int C, uint32_t seed,
@@ -374,7 +384,7 @@ int cg_hash_labels(int32_t *out, const int32_t *vertex, int64_t n_rows, int C, u
     k_hash_labels<<<grid_for(n_rows, 256), 256, 0, (cudaStream_t)stream>>>(out, vertex, n_rows,
                                                                           C, seed);
     CG_CHECK_LAUNCH("k_hash_labels");
-    return 0;
+    return 1;
 }
 
 int cg_copy_rows(int64_t n, int F, const int32_t *src_id, const int32_t *src_row,
@@ -392,7 +402,7 @@ int cg_copy_rows(int64_t n, int F, const int32_t *src_id, const int32_t *src_row
         k_copy_rows<false><<<blocks, threads, 0, (cudaStream_t)stream>>>(
             n, F, src_id, src_row, dst_row, tab, tab_ld, dst, ld_dst);
     CG_CHECK_LAUNCH("k_copy_rows");
-    return 0;
+    return 1;
 }
 
 int cg_spmm(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col, int64_t n_direct,
@@ -425,7 +435,16 @@ int cg_spmm(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col, in
     }
 #undef CG_SPMM_LAUNCH
     CG_CHECK_LAUNCH("k_spmm");
-    return 0;
+    return 1;
+}
+
+int cg_scale_rows(float *X, int64_t ld, int64_t n_rows, int F, const float *scale,
+                  void *stream) {
+    if (n_rows == 0 || F == 0) return 0;
+    k_scale_rows<<<grid_for(n_rows * F, 256), 256, 0, (cudaStream_t)stream>>>(X, ld, n_rows, F,
+                                                                             scale);
+    CG_CHECK_LAUNCH("k_scale_rows");
+    return 1;
 }
 
 int cg_colsum(int64_t M, int N, const float *D, int64_t ldd, float *db, float *ws, void *stream) {
@@ -437,7 +456,7 @@ int cg_colsum(int64_t M, int N, const float *D, int64_t ldd, float *db, float *w
     k_colsum_partial<<<grid, 128, 0, st>>>(M, N, D, ldd, chunk, ws);
     k_reduce_chunks<<<(N + 255) / 256, 256, 0, st>>>(N, nch, ws, db, 0);
     CG_CHECK_LAUNCH("cg_colsum");
-    return 0;
+    return 2;
 }
 
 int cg_softmax_ce(int64_t n_rows, int C, const float *logits, int64_t ld, const int32_t *label,
@@ -449,7 +468,7 @@ int cg_softmax_ce(int64_t n_rows, int C, const float *logits, int64_t ld, const 
                                                                       label, inv_n, grad, ldg, ws);
     k_sum_fixed<<<1, 1024, 0, st>>>(ws, n_rows, loss_out);
     CG_CHECK_LAUNCH("cg_softmax_ce");
-    return 0;
+    return 2;
 }
 
 int cg_adam(int64_t n, float *param, const float *grad, float *m, float *v, float lr,
@@ -460,7 +479,7 @@ int cg_adam(int64_t n, float *param, const float *grad, float *m, float *v, floa
     k_adam<<<grid_for(n, 256, 148 * 8), 256, 0, (cudaStream_t)stream>>>(
         n, param, grad, m, v, lr, beta1, beta2, eps, (float)c1, (float)c2);
     CG_CHECK_LAUNCH("k_adam");
-    return 0;
+    return 1;
 }
 
 int cg_plan_frozen(const cg_plan_static *st, int epoch, int staleness, int me, int32_t *req_ver,
@@ -472,7 +491,7 @@ int cg_plan_frozen(const cg_plan_static *st, int epoch, int staleness, int me, i
         *st, epoch, staleness, me, req_ver, glob_ver, halo_row, stage_src, stage_row, stage_dst,
         gw_slot, counts, flag, staging_base, n_devices, outcome);
     CG_CHECK_LAUNCH("k_plan_frozen");
-    return 0;
+    return 1;
 }
 
 }  // extern "C"

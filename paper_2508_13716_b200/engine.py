@@ -1,0 +1,484 @@
+"""The per-device epoch executor: cache plan -> halo staging -> fused SpMM ->
+transform, loss, backward halo-gradient exchange, K7 all-reduce, Adam.
+
+Everything on the data path is a libcapgnn kernel launched on the current
+torch stream; PyTorch only allocates device memory and provides streams,
+events and torch.distributed.  See DESIGN.md §4-§6.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from ._lib import PlanStatic, call, ptr
+from .comm import HostTier, SoloComm
+from .layout import RunLayout
+from .planner import EpochPlan, SequentialPlanner
+
+GEMM_MODES = {"fp32": 0, "3xtf32": 1, "tf32": 2}
+
+
+def _dev(a, dtype, device):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype).to(device)
+
+
+@dataclass
+class EpochStats:
+    epoch: int
+    loss: float
+    counts: np.ndarray           # (P, 3) local, global, miss
+    seconds: float
+    spmm_fwd_ms: list
+    spmm_bwd_ms: list
+    planner: str                 # "host" or "gpu"
+    flag: int = 0
+    events: tuple | None = None  # (t0, t1) CUDA events when not yet synchronised
+
+
+class Engine:
+    def __init__(self, layout: RunLayout, me: int, kind: str, dims: list[int], bpe: int,
+                 caps, planner: SequentialPlanner, staleness: int, policy: str,
+                 comm=None, lr: float = 0.01, gemm: str = "fp32", params_init=None,
+                 device: int | None = None, freeze_epoch: int | None = None,
+                 record_outcomes: bool = False, plan_mode: str = "auto"):
+        self.L = layout
+        self.me = me
+        self.D = layout.devices[me]
+        self.kind = kind
+        self.dims = list(dims)
+        self.nL = len(dims) - 1
+        self.bpe_f = bpe // 4
+        self.comm = comm or SoloComm()
+        self.planner = planner
+        self.staleness = staleness
+        self.policy = policy
+        self.lr = lr
+        self.gemm_mode = GEMM_MODES[gemm]
+        self.dev = torch.device("cuda", device if device is not None else torch.cuda.current_device())
+        self.record_outcomes = record_outcomes
+        self.plan_mode = plan_mode
+        self.freeze_epoch = freeze_epoch if freeze_epoch is not None else max(1, staleness + 1)
+        self.gpu_plan_ready = False
+        self.step = 0
+        self._alloc(caps, params_init)
+
+    # ------------------------------------------------------------------ setup
+    def _alloc(self, caps, params_init):
+        D, dev, f32, i32, i64 = self.D, self.dev, torch.float32, torch.int32, torch.int64
+        dims = self.dims
+        self.F = dims[:-1]
+        self.C = dims[-1]
+        self.X = [torch.zeros(D.n_rows, F, dtype=f32, device=dev) for F in self.F]
+        self.logits = torch.zeros(D.n_in, self.C, dtype=f32, device=dev)
+        self.Z = [torch.zeros(D.n_in, F, dtype=f32, device=dev) for F in self.F]
+        wmax = max(dims[1:])
+        self.dY = [torch.zeros(D.n_in, wmax, dtype=f32, device=dev) for _ in range(2)]
+        fmax_b = max(self.F[1:], default=4)
+        n_bwd = D.bwd_stage_vertex.size
+        self.G = torch.zeros(D.n_in + n_bwd, fmax_b, dtype=f32, device=dev)
+        self.Hs = torch.zeros(D.n_in, fmax_b, dtype=f32, device=dev) if self.kind == "sage" else None
+        # parameters (flat) + grads (+1 slot for the loss) + Adam state
+        self.pshapes = []
+        for l in range(self.nL):
+            fi, fo = dims[l], dims[l + 1]
+            if self.kind == "gcn":
+                self.pshapes += [(fi, fo), (fo,)]
+            else:
+                self.pshapes += [(fi, fo), (fi, fo), (fo,)]
+        sizes = [int(np.prod(s)) for s in self.pshapes]
+        self.poff = np.concatenate(([0], np.cumsum(sizes))).astype(np.int64)
+        self.n_params = int(self.poff[-1])
+        flat = np.concatenate([np.asarray(p, np.float32).ravel() for p in params_init])
+        assert flat.size == self.n_params
+        self.params = _dev(flat, f32, dev)
+        self.grads = torch.zeros(self.n_params + 1, dtype=f32, device=dev)
+        self.adam_m = torch.zeros(self.n_params, dtype=f32, device=dev)
+        self.adam_v = torch.zeros(self.n_params, dtype=f32, device=dev)
+        ws = 1
+        for l in range(self.nL):
+            ws = max(ws, call("cg_wgrad_workspace", D.n_in, dims[l], dims[l + 1]),
+                     call("cg_wgrad_workspace", D.n_in, 1, dims[l + 1]))
+        self.ws = torch.zeros(ws, dtype=f32, device=dev)
+        self.ce_ws = torch.zeros(max(D.n_in, 1), dtype=f32, device=dev)
+        # graph structure
+        self.fwd_rowptr = _dev(D.fwd_rowptr, i64, dev)
+        self.fwd_col = _dev(D.fwd_col, i32, dev)
+        self.bwd_rowptr = _dev(D.bwd_rowptr, i64, dev)
+        self.bwd_col = _dev(D.bwd_col, i32, dev)
+        self.norm_src = _dev(D.norm_src, f32, dev)
+        self.norm_dst = _dev(D.norm_dst, f32, dev)
+        self.verts32 = _dev(D.verts, i32, dev)
+        self.labels = torch.zeros(D.n_in, dtype=i32, device=dev)
+        st = self.stream()
+        call("cg_hash_labels", ptr(self.labels), ptr(self.verts32), D.n_in, self.C, 1, st)
+        call("cg_hash_features", ptr(self.X[0]), self.F[0], ptr(self.verts32), D.n_in,
+             self.F[0], 0, ptr(self.norm_src) if self.kind == "gcn" else None, st)
+        # per-epoch plan tables (device-level halo positions)
+        nh = max(D.n_halo, 1)
+        self.halo_row = torch.full((nh,), -1, dtype=i32, device=dev)
+        self.stage_src = torch.full((nh,), -1, dtype=i32, device=dev)
+        self.stage_row = torch.zeros(nh, dtype=i32, device=dev)
+        self.stage_dst = torch.full((nh,), -1, dtype=i32, device=dev)
+        self.wb = None  # transient write-back lists (src_id, src_row, dst_row)
+        nu = max(self.L.union.size if self.L.union is not None else 0, 1)
+        self.gw_slot = torch.full((nu,), -1, dtype=i32, device=dev)
+        if self.L.union is not None and self.L.union.size:
+            own = self.L.owner_dev == self.me
+            self.gw_src_id = _dev(np.where(own, self.me, -1), i32, dev)
+            self.gw_src_row = _dev(self.L.owner_row, i32, dev)
+        else:
+            self.gw_src_id = torch.full((1,), -1, dtype=i32, device=dev)
+            self.gw_src_row = torch.zeros(1, dtype=i32, device=dev)
+        # backward staging lists
+        nb = max(n_bwd, 1)
+        self.b_src = _dev(D.bwd_src_dev if n_bwd else [-1], i32, dev)
+        self.b_row = _dev(D.bwd_src_row if n_bwd else [0], i32, dev)
+        self.b_dst = _dev(D.n_in + np.arange(nb), i32, dev)
+        self.n_bwd = n_bwd
+        # host tier (global cache level): c_cpu slots x bpe
+        self.c_cpu = int(caps.c_cpu)
+        self.host = HostTier(self.c_cpu * self.bpe_f * 4, self.comm)
+        self.layer_off = np.concatenate(([0], np.cumsum(self.F))).astype(np.int64)
+        # pointer tables: [X_l on every device..., host tier + layer offset]
+        nd = self.L.n_dev
+        self.tab, self.tab_ld = [], []
+        for l, F in enumerate(self.F):
+            peers = self.comm.exchange_pointers(ptr(self.X[l]), self.dev.index)
+            self.tab.append(_dev(np.array(peers + [self.host.ptr + 4 * int(self.layer_off[l])],
+                                          np.uint64).view(np.int64), torch.int64, dev))
+            self.tab_ld.append(_dev(np.array([F] * nd + [self.bpe_f], np.int64), i64, dev))
+        gpeers = self.comm.exchange_pointers(ptr(self.G), self.dev.index)
+        self.tabG = _dev(np.array(gpeers, np.uint64).view(np.int64), torch.int64, dev)
+        self.tabG_ld = {F: _dev(np.full(nd, F, np.int64), i64, dev) for F in set(self.F)}
+        # frozen-plan (K6) state, created at hand-off
+        self.k6 = None
+        self.loss_dev = torch.zeros(1, dtype=f32, device=dev)
+        torch.cuda.current_stream(self.dev).synchronize()
+
+    def stream(self) -> int:
+        return torch.cuda.current_stream(self.dev).cuda_stream
+
+    def param_views(self) -> list[np.ndarray]:
+        flat = self.params.detach().cpu().numpy()
+        return [flat[self.poff[i]:self.poff[i + 1]].reshape(s) for i, s in enumerate(self.pshapes)]
+
+    def _p(self, i: int) -> int:
+        return ptr(self.params) + 4 * int(self.poff[i])
+
+    def _g(self, i: int) -> int:
+        return ptr(self.grads) + 4 * int(self.poff[i])
+
+    # ------------------------------------------------------------------ plans
+    def _host_tables(self, e: int, plan: EpochPlan, gslot_start: np.ndarray):
+        """Device tables for an epoch planned on the host (any policy)."""
+        L, D, me = self.L, self.D, self.me
+        nd = L.n_dev
+        n_in, nh = D.n_in, D.n_halo
+        halo_row = np.full(max(nh, 1), -1, np.int32)
+        s_src = np.full(max(nh, 1), -1, np.int32)
+        s_row = np.zeros(max(nh, 1), np.int32)
+        s_dst = np.full(max(nh, 1), -1, np.int32)
+        wb_src, wb_dst = [], []
+        if L.union is not None and L.union.size:
+            hoff = L.halo_off
+            for p in D.parts:
+                b, eidx = hoff[p], hoff[p + 1]
+                if eidx == b:
+                    continue
+                hp = D.hpos_off[p]
+                k = np.searchsorted(L.union, D.halo_vertex[hp:hp + (eidx - b)])
+                oc = plan.outcome[b:eidx]
+                ver = plan.version[b:eidx]
+                cur = np.maximum(ver, 1) == e
+                need = D.needed[hp:hp + (eidx - b)]
+                odev = L.owner_dev[k]
+                orow = L.owner_row[k]
+                pos = hp + np.arange(eidx - b)
+                # stale local hit -> read the slab slot in place
+                st_loc = (oc == 0) & ~cur & need
+                halo_row[pos[st_loc]] = D.slab_off[p] + plan.hit_slot[b:eidx][st_loc]
+                # co-resident owner, current value -> read the owner row in place
+                direct = cur & need & (odev == me)
+                halo_row[pos[direct]] = orow[direct]
+                # everything else is staged into its staging row
+                stg = need & ~st_loc & ~direct
+                halo_row[pos[stg]] = n_in + pos[stg]
+                s_dst[pos[stg]] = n_in + pos[stg]
+                from_owner = stg & cur
+                s_src[pos[from_owner]] = odev[from_owner]
+                s_row[pos[from_owner]] = orow[from_owner]
+                from_host = stg & ~cur
+                gsl = gslot_start[k[from_host]]
+                if (gsl < 0).any():
+                    raise RuntimeError("stale global hit without a global slot")
+                s_src[pos[from_host]] = nd
+                s_row[pos[from_host]] = gsl
+                # write-back of the final local-slot contents (after the SpMM)
+                lo, c = int(self.planner.lslot_off[p]), int(self.planner.c_gpu[p])
+                lpos = plan.lslot_pos[lo:lo + c]
+                dirty = plan.lslot_dirty[lo:lo + c].astype(bool)
+                if e == 1:
+                    dirty |= lpos >= 0   # warm (version 0) entries materialise now
+                sl = np.flatnonzero(dirty & (lpos >= 0))
+                if sl.size:
+                    j = lpos[sl]
+                    keep = need[j]
+                    sl, j = sl[keep], j[keep]
+                    wb_dst.append(D.slab_off[p] + sl)
+                    wb_src.append(halo_row[hp + j])
+            # owner-side host-tier writes for this epoch's final global contents
+        gw = np.full(max(L.union.size if L.union is not None else 0, 1), -1, np.int32)
+        if self.c_cpu and L.union is not None and L.union.size:
+            gv = plan.gslot_vertex
+            dirty = plan.gslot_dirty.astype(bool)
+            if e == 1:
+                dirty |= gv >= 0
+            sl = np.flatnonzero(dirty & (gv >= 0))
+            kk = gv[sl]
+            mine = L.owner_dev[kk] == me
+            gw[kk[mine]] = sl[mine]
+        dev = self.dev
+        self.halo_row.copy_(torch.from_numpy(halo_row))
+        self.stage_src.copy_(torch.from_numpy(s_src))
+        self.stage_row.copy_(torch.from_numpy(s_row))
+        self.stage_dst.copy_(torch.from_numpy(s_dst))
+        self.gw_slot.copy_(torch.from_numpy(gw))
+        if wb_dst:
+            d = np.concatenate(wb_dst).astype(np.int32)
+            s = np.concatenate(wb_src).astype(np.int32)
+            self.wb = (_dev(np.full(d.size, me, np.int32), torch.int32, dev),
+                       _dev(s, torch.int32, dev), _dev(d, torch.int32, dev), int(d.size))
+        else:
+            self.wb = None
+
+    def _init_gpu_plan(self):
+        """Hand the frozen membership + versions to K6."""
+        L, pl = self.L, self.planner
+        stt = pl.state()
+        dev, i32 = self.dev, torch.int32
+        # requester tables in K6 order (halo-union major, lookup order)
+        idx = L.req_index
+        slot = stt["req_slot"][idx]
+        part = L.req_part
+        slab_base = np.zeros(L.P, np.int64)
+        for dl in L.devices:
+            for p in dl.parts:
+                slab_base[p] = dl.slab_off[p]
+        req_slot = np.where(slot >= 0, slab_base[part] + slot, -1).astype(np.int32)
+        gslot = stt["gslot"].astype(np.int32)
+        self.k6 = dict(
+            req_off=_dev(L.req_off, torch.int64, dev), req_part=_dev(part, i32, dev),
+            req_dev=_dev(L.req_dev, i32, dev), req_pos=_dev(L.req_pos, i32, dev),
+            req_slot=_dev(req_slot, i32, dev),
+            req_needed=_dev(L.req_needed, torch.uint8, dev),
+            owner_dev=_dev(L.owner_dev, i32, dev), owner_row=_dev(L.owner_row, i32, dev),
+            gslot=_dev(gslot, i32, dev), lfree=_dev(stt["lfree"], i32, dev),
+            score=_dev(pl._score, torch.float64, dev), lmin=_dev(stt["lmin"], torch.float64, dev),
+            req_ver=_dev(stt["req_ver"][idx], i32, dev),
+            glob_ver=_dev(stt["glob_ver"] if stt["glob_ver"].size else [0], i32, dev),
+            counts=torch.zeros(L.P * 3, dtype=torch.int64, device=dev),
+            flag=torch.zeros(1, dtype=i32, device=dev),
+            outcome=torch.zeros(max(idx.size, 1), dtype=torch.int8, device=dev))
+        k = self.k6
+        self.k6_static = PlanStatic(
+            n_union=int(L.union.size), req_off=ptr(k["req_off"]), req_part=ptr(k["req_part"]),
+            req_dev=ptr(k["req_dev"]), req_pos=ptr(k["req_pos"]), req_slot=ptr(k["req_slot"]),
+            req_needed=ptr(k["req_needed"]), owner_dev=ptr(k["owner_dev"]),
+            owner_row=ptr(k["owner_row"]), gslot=ptr(k["gslot"]), lfree=ptr(k["lfree"]),
+            score=ptr(k["score"]), lmin=ptr(k["lmin"]), gmin=float(stt["gmin"]),
+            gfree=int(stt["gfree"]), policy=0 if self.policy == "jaca" else 1, n_parts=L.P)
+        self.gpu_plan_ready = True
+
+    def plan(self, e: int) -> tuple[str, np.ndarray | None, EpochPlan | None]:
+        """Fill this epoch's tables.  Returns (mode, host counts, host plan)."""
+        use_gpu = (self.plan_mode != "host" and self.policy in ("jaca", "fifo")
+                   and e > self.freeze_epoch and self.L.union is not None
+                   and self.L.union.size > 0)
+        if use_gpu and not self.gpu_plan_ready:
+            if self.planner.state()["admissions"] != 0:
+                use_gpu = False   # membership still moving: stay on the host
+            else:
+                self._init_gpu_plan()
+        if use_gpu:
+            k = self.k6
+            k["counts"].zero_()
+            call("cg_plan_frozen", C.addressof(self.k6_static), e, self.staleness, self.me,
+                 ptr(k["req_ver"]), ptr(k["glob_ver"]), ptr(self.halo_row), ptr(self.stage_src),
+                 ptr(self.stage_row), ptr(self.stage_dst), ptr(self.gw_slot), ptr(k["counts"]),
+                 ptr(k["flag"]), self.D.n_in, self.L.n_dev,
+                 ptr(k["outcome"]) if self.record_outcomes else None, self.stream())
+            self.wb = None
+            return "gpu", None, None
+        if self.gpu_plan_ready:
+            raise RuntimeError("host re-planning after the GPU hand-off is not supported")
+        gstart = (self.planner.state()["gslot"] if self.L.union is not None and self.L.union.size
+                  else np.zeros(0, np.int32))
+        plan = self.planner.epoch(e, self.staleness)
+        self._host_tables(e, plan, gstart)
+        return "host", plan.counts.copy(), plan
+
+    # ------------------------------------------------------------------ epoch
+    def _copy(self, n, F, src_id, src_row, dst_row, tab, tab_ld, dst, ld):
+        call("cg_copy_rows", n, F, ptr(src_id), ptr(src_row), ptr(dst_row), ptr(tab),
+             ptr(tab_ld), dst if isinstance(dst, int) else ptr(dst), ld, self.stream())
+
+    def _gw(self, l: int):
+        if self.c_cpu == 0 or self.L.union is None or self.L.union.size == 0:
+            return
+        F = self.F[l]
+        self._copy(self.L.union.size, F, self.gw_src_id, self.gw_src_row, self.gw_slot,
+                   self.tab[l], self.tab_ld[l], self.host.ptr + 4 * int(self.layer_off[l]),
+                   self.bpe_f)
+
+    def run_epoch(self, e: int, timers: bool = True, sync: bool = True) -> EpochStats:
+        D, st, nL, kind = self.D, self.stream(), self.nL, self.kind
+        ev = []
+        mk = (lambda: torch.cuda.Event(enable_timing=True)) if timers else None
+        t0 = mk() if timers else None
+        if timers:
+            t0.record()
+        mode, hcounts, _ = self.plan(e)
+        fwd_ev, bwd_ev = [], []
+        n_in = D.n_in
+        # ---------------- forward
+        for l in range(nL):
+            F, Fo = self.F[l], self.dims[l + 1]
+            if l > 0:
+                self.comm.barrier()
+                self._gw(l - 1)
+            if D.n_halo:
+                self._copy(D.n_halo, F, self.stage_src, self.stage_row, self.stage_dst,
+                           self.tab[l], self.tab_ld[l], self.X[l], F)
+            if timers:
+                a, b = mk(), mk()
+                a.record()
+            call("cg_spmm", n_in, F, ptr(self.fwd_rowptr), ptr(self.fwd_col), n_in,
+                 ptr(self.halo_row), ptr(self.X[l]), F, ptr(self.norm_dst), None, 0, None, 0,
+                 ptr(self.Z[l]), F, st)
+            if timers:
+                b.record()
+                fwd_ev.append((a, b))
+            if self.wb is not None:
+                sid, srow, dst, n = self.wb
+                self._copy(n, F, sid, srow, dst, self.tab[l], self.tab_ld[l], self.X[l], F)
+            last = l == nL - 1
+            out = self.logits if last else self.X[l + 1]
+            if kind == "gcn":
+                call("cg_gemm", n_in, Fo, F, ptr(self.Z[l]), F, self._p(2 * l), 0, None, 0, None,
+                     0, self._p(2 * l + 1), 0 if last else 1,
+                     None if last else ptr(self.norm_src), ptr(out), Fo, self.gemm_mode, st)
+            else:
+                call("cg_gemm", n_in, Fo, F, ptr(self.X[l]), F, self._p(3 * l), F,
+                     ptr(self.Z[l]), F, self._p(3 * l + 1), 0, self._p(3 * l + 2),
+                     0 if last else 1, None, ptr(out), Fo, self.gemm_mode, st)
+        # ---------------- loss
+        n_total = self.L.n
+        dY = self.dY[0]
+        loss_ptr = ptr(self.grads) + 4 * self.n_params
+        call("cg_softmax_ce", n_in, self.C, ptr(self.logits), self.C, ptr(self.labels),
+             1.0 / n_total, ptr(dY), self.C, loss_ptr, ptr(self.ce_ws), st)
+        # ---------------- backward
+        cur = 0
+        for l in range(nL - 1, -1, -1):
+            F, Fo = self.F[l], self.dims[l + 1]
+            dY = self.dY[cur]
+            if kind == "gcn":
+                call("cg_wgrad", n_in, F, Fo, ptr(self.Z[l]), F, ptr(dY), Fo, self._g(2 * l),
+                     ptr(self.ws), self.gemm_mode, st)
+                call("cg_colsum", n_in, Fo, ptr(dY), Fo, self._g(2 * l + 1), ptr(self.ws), st)
+            else:
+                call("cg_wgrad", n_in, F, Fo, ptr(self.X[l]), F, ptr(dY), Fo, self._g(3 * l),
+                     ptr(self.ws), self.gemm_mode, st)
+                call("cg_wgrad", n_in, F, Fo, ptr(self.Z[l]), F, ptr(dY), Fo,
+                     self._g(3 * l + 1), ptr(self.ws), self.gemm_mode, st)
+                call("cg_colsum", n_in, Fo, ptr(dY), Fo, self._g(3 * l + 2), ptr(self.ws), st)
+            if l == 0:
+                break
+            nxt = self.dY[1 - cur]
+            if kind == "gcn":
+                call("cg_gemm", n_in, F, Fo, ptr(dY), Fo, self._p(2 * l), 0, None, 0, None, 1,
+                     None, 0, ptr(self.norm_dst), ptr(self.G), F, self.gemm_mode, st)
+            else:
+                call("cg_gemm", n_in, F, Fo, ptr(dY), Fo, self._p(3 * l + 1), 0, None, 0, None,
+                     1, None, 0, ptr(self.norm_dst), ptr(self.G), F, self.gemm_mode, st)
+                call("cg_gemm", n_in, F, Fo, ptr(dY), Fo, self._p(3 * l), 0, None, 0, None, 1,
+                     None, 0, None, ptr(self.Hs), F, self.gemm_mode, st)
+            self.comm.barrier()
+            if self.n_bwd:
+                self._copy(self.n_bwd, F, self.b_src, self.b_row, self.b_dst, self.tabG,
+                           self.tabG_ld[F], self.G, F)
+            if timers:
+                a, b = mk(), mk()
+                a.record()
+            call("cg_spmm", n_in, F, ptr(self.bwd_rowptr), ptr(self.bwd_col), 1 << 62, None,
+                 ptr(self.G), F, ptr(self.norm_src) if kind == "gcn" else None,
+                 ptr(self.Hs) if kind == "sage" else None, F, ptr(self.X[l]), F, ptr(nxt), F, st)
+            if timers:
+                b.record()
+                bwd_ev.append((a, b))
+            cur = 1 - cur
+        # ---------------- K7 + optimizer
+        self.comm.allreduce_(self.grads)
+        self._gw(nL - 1)
+        self.step += 1
+        call("cg_adam", self.n_params, ptr(self.params), ptr(self.grads), ptr(self.adam_m),
+             ptr(self.adam_v), self.lr, 0.9, 0.999, 1e-8, self.step, st)
+        if timers:
+            t1 = mk()
+            t1.record()
+        stats = EpochStats(epoch=e, loss=float("nan"), counts=hcounts, seconds=0.0,
+                           spmm_fwd_ms=fwd_ev, spmm_bwd_ms=bwd_ev, planner=mode,
+                           events=(t0, t1) if timers else None)
+        if mode == "gpu":
+            # keep this epoch's counters on the device until finish()
+            stats.counts = self.k6["counts"].clone()
+            stats.flag = self.k6["flag"].clone()
+        stats.loss = self.grads[self.n_params:].clone()
+        return self.finish(stats) if sync else stats
+
+    def finish(self, stats: EpochStats) -> EpochStats:
+        """Synchronise one epoch's results to the host (loss, counters, times)."""
+        if not isinstance(stats.loss, float):
+            stats.loss = float(stats.loss.item()) / self.L.n
+        if stats.planner == "gpu" and not isinstance(stats.counts, np.ndarray):
+            stats.counts = stats.counts.view(self.L.P, 3).cpu().numpy()
+            stats.flag = int(stats.flag.item())
+            if stats.flag:
+                raise RuntimeError(
+                    f"epoch {stats.epoch}: frozen-membership precondition violated (an "
+                    "admission would happen); rerun with plan_mode='host'")
+        if stats.events is not None:
+            t0, t1 = stats.events
+            stats.seconds = t0.elapsed_time(t1) / 1e3
+            stats.spmm_fwd_ms = [a.elapsed_time(b) for a, b in stats.spmm_fwd_ms]
+            stats.spmm_bwd_ms = [a.elapsed_time(b) for a, b in stats.spmm_bwd_ms]
+            stats.events = None
+        return stats
+
+    def upload_features(self, host_x) -> None:
+        """H2D copy of this device's input rows (pinned host, raw features),
+        then the GCN source-degree pre-scaling on the device."""
+        D = self.D
+        self.X[0][:D.n_in].copy_(host_x, non_blocking=True)
+        if self.kind == "gcn":
+            call("cg_scale_rows", ptr(self.X[0]), self.F[0], D.n_in, self.F[0],
+                 ptr(self.norm_src), self.stream())
+
+    def gpu_outcomes(self) -> np.ndarray:
+        """Per-requester outcomes of the last GPU-planned epoch (flat order)."""
+        o = self.k6["outcome"].cpu().numpy()[: self.L.req_index.size]
+        out = np.empty_like(o)
+        out[self.L.req_index] = o
+        return out
+
+    def logits_global(self) -> np.ndarray:
+        """This device's logits keyed by vertex id: (verts, logits)."""
+        return self.D.verts, self.logits.detach().cpu().numpy()
+
+    def close(self):
+        self.comm.close()
+        self.host.close()

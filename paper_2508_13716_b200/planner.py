@@ -95,6 +95,7 @@ class SequentialPlanner:
         cnt = np.zeros((P, 3), np.int64)
         call("cg_planner_epoch", self._h, e, staleness, ptr(oc), ptr(ver), ptr(hs), ptr(sa),
              ptr(lp), ptr(ld), ptr(gv), ptr(gd), ptr(cnt))
+        self._last_outcome = oc[:n]
         return EpochPlan(e, oc[:n], ver[:n], hs[:n], sa[:n], lp[:nl], ld[:nl],
                          gv[:self.c_cpu], gd[:self.c_cpu], cnt)
 

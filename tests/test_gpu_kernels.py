@@ -1,0 +1,180 @@
+"""Kernel-level GPU tests through the C ABI (each kernel vs a CPU reference)."""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _t(a, dtype=None):
+    import torch
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype).cuda()
+
+
+def _st():
+    import torch
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _sync():
+    import torch
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("F", [4, 32, 64, 100, 128, 256, 604])
+def test_spmm_with_halo_indirection(F):
+    import torch
+    from paper_2508_13716_b200._lib import call, ptr
+    rng = np.random.default_rng(F)
+    n_rows, n_direct, n_halo, n_extra = 300, 300, 200, 150
+    X = rng.standard_normal((n_direct + n_halo + n_extra, F)).astype(np.float32)
+    deg = rng.integers(0, 40, n_rows)
+    rowptr = np.concatenate(([0], np.cumsum(deg))).astype(np.int64)
+    col = rng.integers(0, n_direct + n_halo, rowptr[-1]).astype(np.int32)
+    halo_row = rng.integers(0, X.shape[0], n_halo).astype(np.int32)
+    scale = rng.random(n_rows).astype(np.float32)
+    add = rng.standard_normal((n_rows, F)).astype(np.float32)
+    mask = rng.standard_normal((n_rows, F)).astype(np.float32)
+    mapped = np.where(col < n_direct, col, halo_row[np.maximum(col - n_direct, 0)])
+    ref = np.zeros((n_rows, F), np.float64)
+    for r in range(n_rows):
+        ref[r] = X[mapped[rowptr[r]:rowptr[r + 1]]].astype(np.float64).sum(0)
+    ref = ref * scale[:, None] + add
+    ref = np.where(mask > 0, ref, 0.0)
+    tX, tr, tc, th = _t(X), _t(rowptr), _t(col), _t(halo_row)
+    ts, ta, tm = _t(scale), _t(add), _t(mask)
+    out = torch.zeros(n_rows, F, device="cuda")
+    call("cg_spmm", n_rows, F, ptr(tr), ptr(tc), n_direct, ptr(th), ptr(tX), F, ptr(ts), ptr(ta),
+         F, ptr(tm), F, ptr(out), F, _st())
+    _sync()
+    np.testing.assert_allclose(out.cpu().numpy(), ref, rtol=1e-5, atol=1e-4)
+
+
+def test_copy_rows_table():
+    import torch
+    from paper_2508_13716_b200._lib import call, ptr
+    rng = np.random.default_rng(1)
+    F = 36
+    srcs = [_t(rng.standard_normal((50, F + 4 * i)).astype(np.float32)) for i in range(3)]
+    tab = _t(np.array([s.data_ptr() for s in srcs], np.uint64).view(np.int64))
+    ld = _t(np.array([F + 4 * i for i in range(3)], np.int64))
+    n = 40
+    sid = rng.integers(-1, 3, n).astype(np.int32)
+    srow = rng.integers(0, 50, n).astype(np.int32)
+    drow = rng.permutation(60)[:n].astype(np.int32)
+    drow[::7] = -1
+    dst = torch.zeros(60, F, device="cuda")
+    keep = [_t(sid), _t(srow), _t(drow)]  # hold the buffers across the async launch
+    call("cg_copy_rows", n, F, ptr(keep[0]), ptr(keep[1]), ptr(keep[2]), ptr(tab), ptr(ld),
+         ptr(dst), F, _st())
+    _sync()
+    exp = np.zeros((60, F), np.float32)
+    for i in range(n):
+        if sid[i] >= 0 and drow[i] >= 0:
+            exp[drow[i]] = srcs[sid[i]].cpu().numpy()[srow[i], :F]
+    assert np.array_equal(dst.cpu().numpy(), exp)
+
+
+@pytest.mark.parametrize("shape", [(1000, 40, 256, 0), (777, 256, 128, 0), (513, 64, 36, 1),
+                                   (2048, 256, 256, 1)])
+def test_gemm_epilogue(shape):
+    import torch
+    from paper_2508_13716_b200._lib import call, ptr
+    M, N, K, tb = shape
+    rng = np.random.default_rng(M)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = rng.standard_normal((N, K) if tb else (K, N)).astype(np.float32)
+    A2 = rng.standard_normal((M, K)).astype(np.float32)
+    B2 = rng.standard_normal((N, K) if tb else (K, N)).astype(np.float32)
+    bias = rng.standard_normal(N).astype(np.float32)
+    rs = rng.random(M).astype(np.float32)
+    Bm = B.T if tb else B
+    B2m = B2.T if tb else B2
+    ref = (A.astype(np.float64) @ Bm + A2.astype(np.float64) @ B2m + bias)
+    ref = np.maximum(ref, 0) * rs[:, None]
+    out = torch.zeros(M, N, device="cuda")
+    k = [_t(A), _t(B), _t(A2), _t(B2), _t(bias), _t(rs)]
+    call("cg_gemm", M, N, K, ptr(k[0]), K, ptr(k[1]), K, ptr(k[2]), K, ptr(k[3]), tb,
+         ptr(k[4]), 1, ptr(k[5]), ptr(out), N, 0, _st())
+    _sync()
+    np.testing.assert_allclose(out.cpu().numpy(), ref, rtol=1e-4, atol=1e-3)
+
+
+def test_wgrad_colsum_deterministic():
+    import torch
+    from paper_2508_13716_b200._lib import call, ptr
+    rng = np.random.default_rng(3)
+    M, K, N = 10000, 128, 40
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    D = rng.standard_normal((M, N)).astype(np.float32)
+    ws = torch.zeros(call("cg_wgrad_workspace", M, K, N), device="cuda")
+    dW = torch.zeros(K, N, device="cuda")
+    db = torch.zeros(N, device="cuda")
+    tA, tD = _t(A), _t(D)
+    call("cg_wgrad", M, K, N, ptr(tA), K, ptr(tD), N, ptr(dW), ptr(ws), 0, _st())
+    call("cg_colsum", M, N, ptr(tD), N, ptr(db), ptr(ws), _st())
+    _sync()
+    np.testing.assert_allclose(dW.cpu().numpy(), A.T.astype(np.float64) @ D, rtol=1e-4, atol=1e-3)
+    np.testing.assert_allclose(db.cpu().numpy(), D.sum(0, dtype=np.float64), rtol=1e-4, atol=1e-3)
+    first = dW.clone()
+    call("cg_wgrad", M, K, N, ptr(tA), K, ptr(tD), N, ptr(dW), ptr(ws), 0, _st())
+    _sync()
+    assert torch.equal(first, dW)
+
+
+def test_softmax_ce_and_adam():
+    import torch
+    from paper_2508_13716_b200._lib import call, ptr
+    rng = np.random.default_rng(4)
+    n, Cc = 3000, 47
+    z = rng.standard_normal((n, Cc)).astype(np.float32) * 3
+    y = rng.integers(0, Cc, n).astype(np.int32)
+    g = torch.zeros(n, Cc, device="cuda")
+    loss = torch.zeros(1, device="cuda")
+    ws = torch.zeros(n, device="cuda")
+    tz, ty = _t(z), _t(y)
+    call("cg_softmax_ce", n, Cc, ptr(tz), Cc, ptr(ty), 1.0 / n, ptr(g), Cc, ptr(loss),
+         ptr(ws), _st())
+    _sync()
+    zz = z.astype(np.float64)
+    m = zz.max(1, keepdims=True)
+    lse = np.log(np.exp(zz - m).sum(1)) + m[:, 0]
+    p = np.exp(zz - lse[:, None])
+    ref_loss = float((lse - zz[np.arange(n), y]).sum())
+    p[np.arange(n), y] -= 1
+    assert abs(loss.item() - ref_loss) <= 1e-5 * abs(ref_loss)
+    np.testing.assert_allclose(g.cpu().numpy(), p / n, rtol=1e-4, atol=1e-8)
+    # Adam, 3 steps vs float64
+    prm = rng.standard_normal(1000).astype(np.float32)
+    tp, tm_, tv = _t(prm), torch.zeros(1000, device="cuda"), torch.zeros(1000, device="cuda")
+    P64, M64, V64 = prm.astype(np.float64), np.zeros(1000), np.zeros(1000)
+    for t in range(1, 4):
+        grad = rng.standard_normal(1000).astype(np.float32)
+        tg = _t(grad)
+        call("cg_adam", 1000, ptr(tp), ptr(tg), ptr(tm_), ptr(tv), 0.01, 0.9, 0.999, 1e-8,
+             t, _st())
+        _sync()
+        M64 = 0.9 * M64 + 0.1 * grad
+        V64 = 0.999 * V64 + 0.001 * grad.astype(np.float64) ** 2
+        P64 -= 0.01 * (M64 / (1 - 0.9 ** t)) / (np.sqrt(V64 / (1 - 0.999 ** t)) + 1e-8)
+    _sync()
+    np.testing.assert_allclose(tp.cpu().numpy(), P64, rtol=1e-5, atol=1e-6)
+
+
+def test_hash_inputs_bit_exact_vs_oracle():
+    import torch
+    from oracle import model_port as omp
+    from paper_2508_13716_b200._lib import call, ptr
+    n, F, Cc = 5000, 100, 47
+    v = _t(np.arange(n, dtype=np.int32))
+    X = torch.zeros(n, F, device="cuda")
+    y = torch.zeros(n, dtype=torch.int32, device="cuda")
+    call("cg_hash_features", ptr(X), F, ptr(v), n, F, 0, None, _st())
+    call("cg_hash_labels", ptr(y), ptr(v), n, Cc, 1, _st())
+    _sync()
+    assert np.array_equal(X.cpu().numpy(), omp.features(n, F, 0))
+    assert np.array_equal(y.cpu().numpy(), omp.labels(n, Cc, 1))

@@ -1,0 +1,89 @@
+"""GPU parity: train() on a B200 vs the CPU oracle, through the C ABI.
+
+Integer parity is exact (per-epoch local/global/miss counts, bytes, trace);
+float parity: per-epoch loss and all-vertex logits within 1e-4 relative
+(fp32 kernels vs the float64 oracle; GEMM mode fp32 SIMT).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from parity_common import oracle_run, rel_err, workload
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+def _train(g, ps, caps, cfg, kind, C, **kw):
+    from paper_2508_13716_b200 import api, hostgraph as H
+    return api.train(g, ps, H.unit_profiles(ps.P), caps, cfg, model=kind, num_classes=C,
+                     keep_logits="all", **kw)
+
+
+CASES = [
+    # kind, n, deg, P, f_dim, C, capacity ("auto" | int), policy, s, epochs
+    ("gcn", 400, 6.0, 4, (16, 32, 32), 7, "auto", "jaca", -1, 4),
+    ("gcn", 400, 6.0, 4, (16, 32), 5, 0, "jaca", -1, 3),
+    ("gcn", 500, 5.0, 3, (16, 32, 32), 6, 60, "jaca", 1, 5),
+    ("gcn", 500, 5.0, 3, (16, 32, 32), 6, 60, "jaca", 0, 4),
+    ("sage", 400, 6.0, 4, (16, 32, 32), 7, "auto", "jaca", -1, 4),
+    ("sage", 500, 5.0, 3, (16, 32), 6, 60, "fifo", 1, 4),
+    ("gcn", 300, 8.0, 2, (8, 16), 4, 40, "lru", -1, 4),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}-P{c[3]}-{c[6]}-{c[7]}-s{c[8]}")
+def test_train_matches_oracle(case):
+    from paper_2508_13716_b200 import hostgraph as H
+    kind, n, deg, P, f_dim, C, cap, policy, s, epochs = case
+    g, ps, og, ops = workload(n, deg, P)
+    if cap == "auto":
+        caps = H.compute_capacities(ps, -1, [180.0] * P, 1024.0, 64.0, 2048.0, f_dim, len(f_dim))
+    else:
+        caps = H.uniform_capacities(ps, cap, f_dim)
+    cfg = H.SimConfig(epochs=epochs, policy=policy, staleness_bound=s, f_dim=f_dim,
+                      L=len(f_dim))
+    rep = _train(g, ps, caps, cfg, kind, C, record_trace=True)
+    pr, outs, _ = oracle_run(og, ops, kind, f_dim, C, caps, policy, s, epochs)
+    # integer parity: counts per (epoch, partition) and the trace
+    for p in pr.plans:
+        got = [(r.local_hits, r.global_hits, r.misses) for r in rep.records if r.epoch == p.epoch]
+        assert got == [tuple(int(x) for x in c) for c in p.counts], p.epoch
+    assert rep.trace_csv == pr.trace_csv(ops.halo)
+    # float parity
+    for e, o in enumerate(outs):
+        assert abs(rep.losses[e] - o.loss) <= TOL * abs(o.loss), (e, rep.losses[e], o.loss)
+        assert rel_err(rep.logits_per_epoch[e], o.logits) <= TOL, e
+
+
+def test_gpu_planner_handoff_matches_host_planner():
+    """K6 (GPU frozen plan) vs the exact host planner on every epoch."""
+    from paper_2508_13716_b200 import hostgraph as H
+    g, ps, og, ops = workload(600, 6.0, 4)
+    f_dim = (16, 16)
+    caps = H.uniform_capacities(ps, 120, f_dim)
+    for s in (-1, 1, 2):
+        cfg = H.SimConfig(epochs=7, policy="jaca", staleness_bound=s, f_dim=f_dim, L=2)
+        a = _train(g, ps, caps, cfg, "gcn", 5, record_trace=True)
+        b = _train(g, ps, caps, cfg, "gcn", 5, record_trace=True, plan_mode="host")
+        assert "gpu" in a.planner and "gpu" not in b.planner
+        assert a.trace_csv == b.trace_csv
+        assert [r.misses for r in a.records] == [r.misses for r in b.records]
+        for x, y in zip(a.logits_per_epoch, b.logits_per_epoch):
+            assert rel_err(x, y) <= TOL
+
+
+def test_bitwise_deterministic_reruns():
+    from paper_2508_13716_b200 import hostgraph as H
+    g, ps, _, _ = workload(500, 6.0, 4)
+    f_dim = (16, 32)
+    caps = H.uniform_capacities(ps, 50, f_dim)
+    cfg = H.SimConfig(epochs=3, policy="jaca", staleness_bound=1, f_dim=f_dim, L=2)
+    a = _train(g, ps, caps, cfg, "gcn", 5)
+    b = _train(g, ps, caps, cfg, "gcn", 5)
+    assert a.losses == b.losses
+    for x, y in zip(a.logits_per_epoch, b.logits_per_epoch):
+        assert np.array_equal(x, y)
