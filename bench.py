@@ -203,7 +203,7 @@ def run_ours(args):
     from paper_2508_13716_b200.models import _unit  # deterministic host features
     rows = D.verts.astype(np.uint64)[:, None]
     host_x = torch.from_numpy(_unit(0, rows, np.arange(F_DIM[0], dtype=np.uint64)[None, :])).pin_memory()
-    host_logits = torch.empty(D.n_in, CLASSES).pin_memory()
+    host_logits = torch.empty(D.n_in, eng.C4).pin_memory()
     host_loss = torch.empty(1).pin_memory()
     barrier()
     torch.cuda.synchronize()
@@ -359,7 +359,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--parts", type=int, default=PARTS)
     ap.add_argument("--staleness", type=int, default=-1)
-    ap.add_argument("--gemm", default="fp32", choices=["fp32", "3xtf32", "tf32"])
+    ap.add_argument("--gemm", default="3xtf32", choices=["fp32", "3xtf32", "tf32"])
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-budget", type=float, default=150.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

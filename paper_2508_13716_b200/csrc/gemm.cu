@@ -21,6 +21,8 @@ int cg_gemm_tc(int64_t M, int N, int K1, const float *A1, int64_t lda1, const fl
                const float *A2, int64_t lda2, const float *B2, int trans_b, const float *bias,
                int relu, const float *row_scale, float *C, int64_t ldc, int mode,
                cudaStream_t st);
+int cg_wgrad_tc(int64_t M, int K, int N, const float *A, int64_t lda, const float *D, int64_t ldd,
+                float *ws, int64_t chunk, int64_t n_chunks, int mode, cudaStream_t st);
 
 namespace {
 
@@ -163,7 +165,7 @@ __global__ void k_wgrad_reduce(int64_t n_out, int64_t n_chunks, const float *__r
     out[i] = s;
 }
 
-constexpr int64_t kWgradChunk = 4096;
+constexpr int64_t kWgradChunk = 1024;  // short TC accumulation chains (accuracy), many CTAs
 
 }  // namespace
 
@@ -191,17 +193,24 @@ int64_t cg_wgrad_workspace(int64_t M, int K, int N) {
 
 int cg_wgrad(int64_t M, int K, int N, const float *A, int64_t lda, const float *D, int64_t ldd,
              float *dW, float *ws, int mode, void *stream) {
-    (void)mode;
     if (K == 0 || N == 0) return 0;
     cudaStream_t st = (cudaStream_t)stream;
     int64_t nch = (M + kWgradChunk - 1) / kWgradChunk;
     if (nch < 1) nch = 1;
-    dim3 grid((K + WK - 1) / WK, (N + WN - 1) / WN, (unsigned)nch);
-    k_wgrad_partial<<<grid, 256, 0, st>>>(M, K, N, A, lda, D, ldd, kWgradChunk, ws);
+    int launched = 0;
+    if (mode == 1 || mode == 2) {
+        int rc = cg_wgrad_tc(M, K, N, A, lda, D, ldd, ws, kWgradChunk, nch, mode, st);
+        if (rc < 0) return rc;
+        launched += rc;
+    } else {
+        dim3 grid((K + WK - 1) / WK, (N + WN - 1) / WN, (unsigned)nch);
+        k_wgrad_partial<<<grid, 256, 0, st>>>(M, K, N, A, lda, D, ldd, kWgradChunk, ws);
+        launched += 1;
+    }
     int64_t n_out = (int64_t)K * N;
     k_wgrad_reduce<<<(unsigned)((n_out + 255) / 256), 256, 0, st>>>(n_out, nch, ws, dW);
     cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? 2 : cg_cuda_fail(e, "cg_wgrad");
+    return e == cudaSuccess ? launched + 1 : cg_cuda_fail(e, "cg_wgrad");
 }
 
 }  // extern "C"

@@ -1,12 +1,554 @@
-// K5 tensor-core path (tcgen05): placeholder until the sm_100a kernel lands.
+// K5 on the 5th-generation tensor cores (sm_100a): tcgen05.mma kind::tf32
+// with TMA-loaded, 128B-swizzled operand tiles and the accumulator in TMEM.
+//
+//   mode 1 = 3xTF32 (parity): a*b ~= a_hi*b_hi + a_hi*b_lo + a_lo*b_hi where
+//            x_hi = x with the low 13 mantissa bits cleared and x_lo = x - x_hi,
+//            split in shared memory by the epilogue warps while the TMA
+//            producer runs ahead -- ~fp32 accuracy at 3 MMAs per k-step;
+//   mode 2 = 1xTF32 (fast mode, stated looser bound).
+//
+// One CTA computes a 128 x BN (BN <= 128) output tile.  Warp roles:
+//   warp 0      TMA producer (one elected lane)
+//   warp 1      TMEM allocator + MMA issuer (one elected lane)
+//   warps 4..7  operand splitters (3xTF32) and the epilogue: TMEM -> regs ->
+//               bias / ReLU / row-scale -> global (warp w%4 owns TMEM lanes
+//               32*(w%4) .. +31, i.e. output rows)
+// Operands may be K-major or MN-major (both are legal for kind::tf32 on
+// sm_100), so every GEMM of the layer -- forward Z.W, input gradient
+// dY.W^T and the weight gradient Z^T.dY (both operands MN-major, reduced
+// over a deterministic split of the long vertex axis) -- reads its operands
+// straight from the row-major activation buffers, with no transposes.
+
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
-#include <string>
-extern void cg_set_error(const std::string &msg);
 
-int cg_gemm_tc(int64_t, int, int, const float *, int64_t, const float *, int, const float *,
-               int64_t, const float *, int, const float *, int, const float *, float *, int64_t,
-               int mode, cudaStream_t) {
-    cg_set_error("cg_gemm: tensor-core mode " + std::to_string(mode) + " not built");
-    return -1;
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "../../include/capgnn.h"
+
+extern void cg_set_error(const std::string &msg);
+extern int cg_cuda_fail(cudaError_t e, const char *what);
+
+namespace tc {
+
+constexpr int BM = 128;          // UMMA M (cta_group::1)
+constexpr int BK = 32;           // fp32 elements per 128-byte swizzle row
+constexpr int UK = 8;            // K per tcgen05.mma kind::tf32
+constexpr int BN_MAX = 128;
+constexpr int TILE_BYTES = BM * BK * 4;          // 16 KB, A or B operand stage
+constexpr int STAGE_BYTES_1X = 2 * TILE_BYTES;   // A + B
+constexpr int STAGE_BYTES_3X = 4 * TILE_BYTES;   // A, B, A_lo, B_lo
+constexpr int THREADS = 384;  // 12 warps: TMA, MMA, -, -, 4 epilogue, 4 splitter
+
+struct Op {
+    int K;           // reduction extent of this operand pair
+    int a_mn, b_mn;  // 1 = MN-major
+};
+
+struct Params {
+    int64_t M;       // rows of the output tile space (GEMM M)
+    int N;           // GEMM N
+    int n_ops;
+    Op op[2];
+    int64_t k_chunk;  // split-K: reduction elements per blockIdx.z (0 = all)
+    const float *bias;
+    int relu;
+    const float *row_scale;
+    float *C;
+    int64_t ldc;
+    int split3;      // 3xTF32
+    int stages;
+    int BN;          // UMMA N (multiple of 16, <= 128)
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done = 0;
+    const uint32_t a = smem_u32(bar);
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap *map, uint64_t *bar, void *dst,
+                                            int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// UMMA shared-memory descriptor (sm_100 version bits).  Layout type 2 is the
+// 128B swizzle (K-major operands); type 1 is 128B swizzle with 32-byte
+// atomicity, the only MN-major layout kind::tf32 accepts.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo,
+                                              uint32_t layout) {
+    return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | ((uint64_t)layout << 61);
+}
+
+// Instruction descriptor: D f32, A/B tf32, majors, N, M.
+__device__ __forceinline__ uint32_t instr_desc(int a_mn, int b_mn, int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) |
+           ((uint32_t)b_mn << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+          "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Tile t of the persistent schedule -> (m tile, n tile, split-K chunk);
+// consecutive t share the m tile so concurrently running CTAs reuse the A
+// rows through L2.
+struct TileCoord {
+    int64_t m0;
+    int n0;
+    int z;
+};
+
+__device__ __forceinline__ TileCoord tile_of(const Params &p, int64_t t, int n_tiles,
+                                             int64_t m_tiles) {
+    TileCoord c;
+    const int64_t per_z = m_tiles * n_tiles;
+    c.z = (int)(t / per_z);
+    const int64_t r = t - (int64_t)c.z * per_z;
+    c.m0 = (r / n_tiles) * BM;
+    c.n0 = (int)(r % n_tiles) * p.BN;
+    return c;
+}
+
+__device__ __forceinline__ void kblocks(const Params &p, int o, int z, int &begin, int &count) {
+    int64_t k_lo = 0, k_hi = p.op[o].K;
+    if (p.k_chunk > 0) {
+        k_lo = (int64_t)z * p.k_chunk;
+        k_hi = (k_lo + p.k_chunk < k_hi) ? k_lo + p.k_chunk : k_hi;
+    }
+    begin = (int)(k_lo / BK);
+    count = k_hi > k_lo ? (int)((k_hi - k_lo + BK - 1) / BK) : 0;
+}
+
+// Persistent warp-specialised kernel: the smem stage ring and the two TMEM
+// accumulator buffers run continuously across this CTA's tiles, so the
+// epilogue of tile i overlaps the TMA + MMA of tile i+1.
+__global__ void __launch_bounds__(THREADS, 1)
+k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mB0,
+          const __grid_constant__ CUtensorMap mA1, const __grid_constant__ CUtensorMap mB1,
+          const Params p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int S = p.stages;
+    const int stage_bytes = p.split3 ? STAGE_BYTES_3X : STAGE_BYTES_1X;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + S * stage_bytes);
+    uint64_t *conv = full + S;
+    uint64_t *empty = conv + S;
+    uint64_t *tfull = empty + S;   // [2] accumulator ready
+    uint64_t *tempty = tfull + 2;  // [2] accumulator drained
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int n_tiles = (p.N + p.BN - 1) / p.BN;
+    const int64_t m_tiles = (p.M + BM - 1) / BM;
+    const int64_t n_z = p.k_chunk > 0 ? (p.op[0].K + p.k_chunk - 1) / p.k_chunk : 1;
+    const int64_t total_tiles = m_tiles * n_tiles * n_z;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&conv[s], 128);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(256));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem_base = *tmem_slot;
+    const int nb_b = (p.BN + 31) / 32;  // 32-column boxes for an MN-major B
+
+    if (warp == 0 && lane == 0) {
+        // ------------------------------------------------ TMA producer
+        uint32_t it = 0;
+        for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+            const TileCoord tc = tile_of(p, t, n_tiles, m_tiles);
+            for (int o = 0; o < p.n_ops; ++o) {
+                int kb0, nkb;
+                kblocks(p, o, tc.z, kb0, nkb);
+                const CUtensorMap *ma = o ? &mA1 : &mA0;
+                const CUtensorMap *mb = o ? &mB1 : &mB0;
+                const uint32_t bbytes = p.op[o].b_mn ? nb_b * 32 * BK * 4 : p.BN * BK * 4;
+                for (int kb = kb0; kb < kb0 + nkb; ++kb, ++it) {
+                    const int s = it % S;
+                    mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+                    const int k0 = kb * BK;
+                    uint8_t *sa = smem + s * stage_bytes;
+                    uint8_t *sb = sa + TILE_BYTES;
+                    mbar_expect_tx(&full[s], TILE_BYTES + bbytes);
+                    if (p.op[o].a_mn) {
+                        for (int b = 0; b < 4; ++b)
+                            tma_load_2d(ma, &full[s], sa + b * 4096, (int)(tc.m0 + 32 * b), k0);
+                    } else {
+                        tma_load_2d(ma, &full[s], sa, k0, (int)tc.m0);
+                    }
+                    if (p.op[o].b_mn) {
+                        for (int b = 0; b < nb_b; ++b)
+                            tma_load_2d(mb, &full[s], sb + b * 4096, tc.n0 + 32 * b, k0);
+                    } else {
+                        tma_load_2d(mb, &full[s], sb, k0, tc.n0);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ------------------------------------------------ MMA issuer
+        uint32_t it = 0, ti = 0;
+        for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++ti) {
+            const TileCoord tc = tile_of(p, t, n_tiles, m_tiles);
+            const uint32_t acc_buf = ti & 1;
+            mbar_wait(&tempty[acc_buf], ((ti >> 1) & 1) ^ 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t tmem_d = tmem_base + acc_buf * 128;
+            bool first = true;
+            for (int o = 0; o < p.n_ops; ++o) {
+                int kb0, nkb;
+                kblocks(p, o, tc.z, kb0, nkb);
+                const int a_mn = p.op[o].a_mn, b_mn = p.op[o].b_mn;
+                const uint32_t idesc = instr_desc(a_mn, b_mn, p.BN);
+                // K-major (SW128): 8-row x 128 B atoms, SBO = 1024, k-step = +32 B.
+                // MN-major (SW128, 32 B atoms): 4-row x 128 B atoms, SBO = 512
+                // between K groups, LBO = 4096 between the 32-wide MN boxes,
+                // k-step = +1024 B.
+                const uint32_t a_lbo = a_mn ? 4096 : 16, b_lbo = b_mn ? 4096 : 16;
+                const uint32_t a_sbo = a_mn ? 512 : 1024, b_sbo = b_mn ? 512 : 1024;
+                const uint32_t a_lay = a_mn ? 1u : 2u, b_lay = b_mn ? 1u : 2u;
+                const uint32_t a_step = a_mn ? 1024 : 32, b_step = b_mn ? 1024 : 32;
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int s = it % S;
+                    const uint32_t ph = (it / S) & 1;
+                    if (p.split3) mbar_wait(&conv[s], ph);
+                    else mbar_wait(&full[s], ph);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t sa = smem_u32(smem + s * stage_bytes);
+                    const uint32_t sb = sa + TILE_BYTES;
+                    const uint32_t sa_lo = sa + 2 * TILE_BYTES, sb_lo = sa + 3 * TILE_BYTES;
+#pragma unroll
+                    for (int j = 0; j < BK / UK; ++j) {
+                        const uint64_t da = smem_desc(sa + j * a_step, a_lbo, a_sbo, a_lay);
+                        const uint64_t db = smem_desc(sb + j * b_step, b_lbo, b_sbo, b_lay);
+                        const uint32_t acc0 = first ? 0u : 1u;
+                        first = false;
+                        if (p.split3) {
+                            const uint64_t dal = smem_desc(sa_lo + j * a_step, a_lbo, a_sbo, a_lay);
+                            const uint64_t dbl = smem_desc(sb_lo + j * b_step, b_lbo, b_sbo, b_lay);
+                            mma_tf32(tmem_d, dal, db, idesc, acc0);
+                            mma_tf32(tmem_d, da, dbl, idesc, 1u);
+                            mma_tf32(tmem_d, da, db, idesc, 1u);
+                        } else {
+                            mma_tf32(tmem_d, da, db, idesc, acc0);
+                        }
+                    }
+                    mma_commit(&empty[s]);  // frees the smem slot once these MMAs retire
+                }
+            }
+            mma_commit(&tfull[acc_buf]);
+        }
+    } else if (warp >= 4 && warp < 8) {
+        // ------------------------------------------------ epilogue
+        const int q = warp & 3;
+        uint32_t ti = 0;
+        for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++ti) {
+            const TileCoord tc = tile_of(p, t, n_tiles, m_tiles);
+            const uint32_t acc_buf = ti & 1;
+            mbar_wait(&tfull[acc_buf], (ti >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const int64_t row = tc.m0 + 32 * q + lane;
+            const bool live = row < p.M;
+            const float rs = (p.row_scale && live) ? p.row_scale[row] : 1.f;
+            float *crow = p.k_chunk > 0 ? p.C + ((int64_t)tc.z * p.M + row) * p.ldc
+                                        : p.C + row * p.ldc;
+            const bool vec = ((p.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0);
+            for (int c0 = 0; c0 < p.BN; c0 += 32) {
+                float v[32];
+                tmem_ld32(tmem_base + acc_buf * 128 + ((uint32_t)(32 * q) << 16) + c0, v);
+                if (!live) continue;
+#pragma unroll
+                for (int i = 0; i < 32; i += 4) {
+                    const int n = tc.n0 + c0 + i;
+                    float x[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        float y = v[i + u];
+                        if (p.bias && n + u < p.N) y += p.bias[n + u];
+                        if (p.relu) y = fmaxf(y, 0.f);
+                        x[u] = y * rs;
+                    }
+                    if (vec && n + 3 < p.N && c0 + i + 3 < p.BN) {
+                        *reinterpret_cast<float4 *>(crow + n) = make_float4(x[0], x[1], x[2], x[3]);
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (n + u < p.N && c0 + i + u < p.BN) crow[n + u] = x[u];
+                    }
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            mbar_arrive(&tempty[acc_buf]);
+        }
+    } else if (warp >= 8 && p.split3) {
+        // ------------------------------------------------ hi/lo split (3xTF32)
+        const int t128 = threadIdx.x - 256;
+        uint32_t it = 0;
+        for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+            const TileCoord tc = tile_of(p, t, n_tiles, m_tiles);
+            for (int o = 0; o < p.n_ops; ++o) {
+                int kb0, nkb;
+                kblocks(p, o, tc.z, kb0, nkb);
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int s = it % S;
+                    mbar_wait(&full[s], (it / S) & 1);
+                    uint4 *hi = reinterpret_cast<uint4 *>(smem + s * stage_bytes);
+                    uint4 *lo = reinterpret_cast<uint4 *>(smem + s * stage_bytes + 2 * TILE_BYTES);
+#pragma unroll 4
+                    for (int i = t128; i < 2 * TILE_BYTES / 16; i += 128) {
+                        uint4 w = hi[i];
+                        uint4 h = make_uint4(w.x & 0xFFFFE000u, w.y & 0xFFFFE000u,
+                                             w.z & 0xFFFFE000u, w.w & 0xFFFFE000u);
+                        uint4 l = make_uint4(
+                            __float_as_uint(__uint_as_float(w.x) - __uint_as_float(h.x)),
+                            __float_as_uint(__uint_as_float(w.y) - __uint_as_float(h.y)),
+                            __float_as_uint(__uint_as_float(w.z) - __uint_as_float(h.z)),
+                            __float_as_uint(__uint_as_float(w.w) - __uint_as_float(h.w)));
+                        hi[i] = h;
+                        lo[i] = l;
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_arrive(&conv[s]);
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                     "r"(256));
+    }
+}
+
+// ------------------------------------------------------------------ host
+
+typedef CUresult (*encode_fn_t)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+encode_fn_t encoder() {
+    static encode_fn_t fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            p)
+            fn = reinterpret_cast<encode_fn_t>(p);
+    }
+    return fn;
+}
+
+// 2-D fp32 tensor [outer x inner] with row stride ld (elements), box {32, box_outer}.
+bool make_map(CUtensorMap *m, const float *ptr, int64_t inner, int64_t outer, int64_t ld,
+              int box_outer, bool mn_major) {
+    encode_fn_t enc = encoder();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+    cuuint32_t box[2] = {32u, (cuuint32_t)box_outer};
+    cuuint32_t estr[2] = {1u, 1u};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(ptr), dims, strides,
+               box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int launch(const Params &p0, const CUtensorMap &a0, const CUtensorMap &b0, const CUtensorMap &a1,
+           const CUtensorMap &b1, int grid_z, cudaStream_t st) {
+    Params p = p0;
+    const int stage_bytes = p.split3 ? STAGE_BYTES_3X : STAGE_BYTES_1X;
+    p.stages = p.split3 ? 3 : 6;
+    const size_t smem = (size_t)p.stages * stage_bytes + 1024 + 512;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)(6 * STAGE_BYTES_1X + 1024 + 512));
+        if (e != cudaSuccess) return cg_cuda_fail(e, "cudaFuncSetAttribute(k_gemm_tc)");
+        attr_set = true;
+    }
+    static int n_sm = 0;
+    if (!n_sm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+        if (n_sm <= 0) n_sm = 148;
+    }
+    const int64_t tiles = (int64_t)((p.N + p.BN - 1) / p.BN) * ((p.M + BM - 1) / BM) * grid_z;
+    const unsigned grid = (unsigned)(tiles < n_sm ? tiles : n_sm);   // persistent
+    k_gemm_tc<<<grid, THREADS, smem, st>>>(a0, b0, a1, b1, p);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 1 : cg_cuda_fail(e, "k_gemm_tc");
+}
+
+inline int bn_for(int N) {
+    int bn = N < BN_MAX ? ((N + 15) / 16) * 16 : BN_MAX;
+    return bn < 16 ? 16 : bn;
+}
+
+}  // namespace tc
+
+// C = epi(A1 B1 + A2 B2): A row-major [M x K] (K-major), B either [K x N]
+// row-major (MN-major, trans_b = 0) or [N x K] row-major (K-major, trans_b = 1).
+int cg_gemm_tc(int64_t M, int N, int K1, const float *A1, int64_t lda1, const float *B1, int K2,
+               const float *A2, int64_t lda2, const float *B2, int trans_b, const float *bias,
+               int relu, const float *row_scale, float *C, int64_t ldc, int mode,
+               cudaStream_t st) {
+    using namespace tc;
+    if (mode != 1 && mode != 2) {
+        cg_set_error("cg_gemm: unknown mode");
+        return -1;
+    }
+    if ((lda1 % 4) || (A2 && lda2 % 4) || (trans_b ? (K1 % 4) : (N % 4)) ||
+        ((uintptr_t)A1 % 16) || ((uintptr_t)B1 % 16)) {
+        cg_set_error("cg_gemm_tc: operands must be 16-byte aligned with ld % 4 == 0");
+        return -1;
+    }
+    Params p{};
+    p.M = M;
+    p.N = N;
+    p.BN = bn_for(N);
+    p.split3 = mode == 1;
+    p.bias = bias;
+    p.relu = relu;
+    p.row_scale = row_scale;
+    p.C = C;
+    p.ldc = ldc;
+    p.k_chunk = 0;
+    CUtensorMap ma[2], mb[2];
+    const float *As[2] = {A1, A2};
+    const float *Bs[2] = {B1, B2};
+    const int Ks[2] = {K1, K2};
+    const int64_t ldas[2] = {lda1, lda2};
+    p.n_ops = (A2 && K2 > 0) ? 2 : 1;
+    for (int o = 0; o < p.n_ops; ++o) {
+        p.op[o].K = Ks[o];
+        p.op[o].a_mn = 0;
+        p.op[o].b_mn = trans_b ? 0 : 1;
+        bool ok = make_map(&ma[o], As[o], Ks[o], M, ldas[o], BM, false);
+        ok = ok && (trans_b ? make_map(&mb[o], Bs[o], Ks[o], N, Ks[o], p.BN, false)
+                            : make_map(&mb[o], Bs[o], N, Ks[o], N, 32, true));
+        if (!ok) {
+            cg_set_error("cg_gemm_tc: cuTensorMapEncodeTiled failed");
+            return -1;
+        }
+    }
+    if (p.n_ops == 1) {
+        ma[1] = ma[0];
+        mb[1] = mb[0];
+    }
+    return launch(p, ma[0], mb[0], ma[1], mb[1], 1, st);
+}
+
+// Partial weight gradients: ws[c][k][n] = sum_{m in chunk c} A[m, k] D[m, n].
+int cg_wgrad_tc(int64_t M, int K, int N, const float *A, int64_t lda, const float *D, int64_t ldd,
+                float *ws, int64_t chunk, int64_t n_chunks, int mode, cudaStream_t st) {
+    using namespace tc;
+    if ((lda % 4) || (ldd % 4) || ((uintptr_t)A % 16) || ((uintptr_t)D % 16)) {
+        cg_set_error("cg_wgrad_tc: operands must be 16-byte aligned with ld % 4 == 0");
+        return -1;
+    }
+    Params p{};
+    p.M = K;          // output rows = input features
+    p.N = N;
+    p.BN = bn_for(N);
+    p.split3 = mode == 1;
+    p.n_ops = 1;
+    p.op[0].K = (int)M;  // reduction over vertices
+    p.op[0].a_mn = 1;
+    p.op[0].b_mn = 1;
+    p.k_chunk = chunk;
+    p.C = ws;
+    p.ldc = N;
+    CUtensorMap ma, mb;
+    if (!make_map(&ma, A, K, M, lda, BK, true) || !make_map(&mb, D, N, M, ldd, BK, true)) {
+        cg_set_error("cg_wgrad_tc: cuTensorMapEncodeTiled failed");
+        return -1;
+    }
+    return launch(p, ma, mb, ma, mb, (int)n_chunks, st);
 }

@@ -77,21 +77,36 @@ __global__ void k_copy_rows(int64_t n, int F, const int32_t *__restrict__ src_id
                             const float *const *__restrict__ tab,
                             const int64_t *__restrict__ tab_ld, float *__restrict__ dst,
                             int64_t ld_dst) {
+    // Each warp scans 32 table entries at a time (one per lane), compacts the
+    // live ones with a ballot, then copies those rows cooperatively: most
+    // epochs most entries are "nothing to move" (stale local hits).
     const int lane = threadIdx.x & (kWarp - 1);
     int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / kWarp;
     int64_t nwarps = (int64_t)gridDim.x * blockDim.x / kWarp;
-    for (int64_t i = warp; i < n; i += nwarps) {
-        int sid = src_id[i];
-        int drow = dst_row[i];
-        if (sid < 0 || drow < 0) continue;
-        const float *s = tab[sid] + (int64_t)src_row[i] * tab_ld[sid];
-        float *d = dst + (int64_t)drow * ld_dst;
-        if (VEC) {
-            const float4 *s4 = reinterpret_cast<const float4 *>(s);
-            float4 *d4 = reinterpret_cast<float4 *>(d);
-            for (int c = lane; c < (F >> 2); c += kWarp) d4[c] = s4[c];
-        } else {
-            for (int c = lane; c < F; c += kWarp) d[c] = s[c];
+    for (int64_t base = warp * kWarp; base < n; base += nwarps * kWarp) {
+        const int64_t i = base + lane;
+        int sid = -1, srow = 0, drow = -1;
+        if (i < n) {
+            sid = src_id[i];
+            drow = dst_row[i];
+            if (sid >= 0 && drow >= 0) srow = src_row[i];
+        }
+        unsigned live = __ballot_sync(0xffffffffu, sid >= 0 && drow >= 0);
+        while (live) {
+            const int j = __ffs(live) - 1;
+            live &= live - 1;
+            const int s = __shfl_sync(0xffffffffu, sid, j);
+            const int r = __shfl_sync(0xffffffffu, srow, j);
+            const int d = __shfl_sync(0xffffffffu, drow, j);
+            const float *sp = tab[s] + (int64_t)r * tab_ld[s];
+            float *dp = dst + (int64_t)d * ld_dst;
+            if (VEC) {
+                const float4 *s4 = reinterpret_cast<const float4 *>(sp);
+                float4 *d4 = reinterpret_cast<float4 *>(dp);
+                for (int c = lane; c < (F >> 2); c += kWarp) d4[c] = s4[c];
+            } else {
+                for (int c = lane; c < F; c += kWarp) dp[c] = sp[c];
+            }
         }
     }
 }
@@ -232,16 +247,52 @@ __global__ void k_sum_fixed(const float *__restrict__ x, int64_t n, float *__res
     if (threadIdx.x == 0) *out = (float)sh[0];
 }
 
-// Column sums over m in fixed chunks: ws[chunk][n], then fixed-order reduce.
-__global__ void k_colsum_partial(int64_t M, int N, const float *__restrict__ D, int64_t ldd,
-                                 int64_t chunk, float *__restrict__ ws) {
-    int n = blockIdx.x * blockDim.x + threadIdx.x;
-    int64_t c = blockIdx.y;
-    if (n >= N) return;
-    int64_t m0 = c * chunk, m1 = min(M, m0 + chunk);
+// Column sums over m in fixed chunks of kColChunk rows: lanes own columns
+// (coalesced 128 B rows), the 8 warps of a block take interleaved rows, and
+// the 8 per-warp sums are combined in a fixed order -> ws[chunk][n].
+constexpr int kColChunk = 256;
+__global__ void __launch_bounds__(256)
+k_colsum_partial(int64_t M, int N, const float *__restrict__ D, int64_t ldd,
+                 float *__restrict__ ws) {
+    __shared__ float part[8][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int n = blockIdx.x * 32 + lane;
+    const int64_t m0 = (int64_t)blockIdx.y * kColChunk;
+    const int64_t m1 = min(M, m0 + kColChunk);
     float s = 0.f;
-    for (int64_t m = m0; m < m1; ++m) s += D[m * ldd + n];
-    ws[c * N + n] = s;
+    if (n < N) {
+#pragma unroll 8
+        for (int64_t m = m0 + w; m < m1; m += 8) s += D[m * ldd + n];
+    }
+    part[w][lane] = s;
+    __syncthreads();
+    if (w == 0 && n < N) {
+        float t = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) t += part[k][lane];
+        ws[blockIdx.y * (int64_t)N + n] = t;
+    }
+}
+
+// out[i] = sum_c ws[c][i], fixed order: 8 warps stride the chunks, then a
+// fixed combination of the 8 partials.
+__global__ void __launch_bounds__(256)
+k_reduce_chunks_tree(int64_t n_out, int64_t n_chunks, const float *__restrict__ ws,
+                     float *__restrict__ out) {
+    __shared__ float part[8][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t i = blockIdx.x * 32 + lane;
+    float s = 0.f;
+    if (i < n_out)
+        for (int64_t c = w; c < n_chunks; c += 8) s += ws[c * n_out + i];
+    part[w][lane] = s;
+    __syncthreads();
+    if (w == 0 && i < n_out) {
+        float t = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) t += part[k][lane];
+        out[i] = t;
+    }
 }
 
 __global__ void k_reduce_chunks(int64_t n_out, int64_t n_chunks, const float *__restrict__ ws,
@@ -285,13 +336,13 @@ __device__ __forceinline__ bool fresh(int32_t ver, int e, int s) { return s < 0 
 // reference's global lookup order (position in the requester's halo, then
 // partition slot), which is the only order that matters for u because,
 // with frozen membership, a lookup of u touches only u's own entries.
-__global__ void k_plan_frozen(cg_plan_static st, int e, int s, int me, int32_t *req_ver,
-                              int32_t *glob_ver, int32_t *halo_row, int32_t *stage_src,
-                              int32_t *stage_row, int32_t *stage_dst, int32_t *gw_slot,
-                              int64_t *counts, int32_t *flag, int32_t staging_base,
-                              int32_t n_devices, int8_t *outcome) {
-    int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (u >= st.n_union) return;
+__device__ __forceinline__ void plan_vertex(const cg_plan_static &st, int64_t u, int e, int s,
+                                            int me, int32_t *req_ver, int32_t *glob_ver,
+                                            int32_t *halo_row, int32_t *stage_src,
+                                            int32_t *stage_row, int32_t *stage_dst,
+                                            int32_t *gw_slot, unsigned int *tally,
+                                            int32_t *flag, int32_t staging_base,
+                                            int32_t n_devices, int8_t *outcome) {
     const int32_t g = st.gslot[u];
     const int32_t odev = st.owner_dev[u], orow = st.owner_row[u];
     bool gdirty = false;
@@ -318,7 +369,7 @@ __global__ void k_plan_frozen(cg_plan_static st, int e, int s, int me, int32_t *
                 *flag = 1;
         }
         if (outcome) outcome[k] = (int8_t)oc;
-        atomicAdd(reinterpret_cast<unsigned long long *>(counts + 3 * part + oc), 1ull);
+        atomicAdd(&tally[3 * part + oc], 1u);
         if (st.req_dev[k] != me) continue;
         const int32_t pos = st.req_pos[k];
         const bool cur = (ver < 1 ? 1 : ver) == e;
@@ -358,6 +409,28 @@ __global__ void k_plan_frozen(cg_plan_static st, int e, int s, int me, int32_t *
     }
 }
 
+
+constexpr int kPlanMaxParts = 256;
+__global__ void __launch_bounds__(256)
+k_plan_frozen(cg_plan_static st, int e, int s, int me, int32_t *req_ver,
+              int32_t *glob_ver, int32_t *halo_row, int32_t *stage_src,
+              int32_t *stage_row, int32_t *stage_dst, int32_t *gw_slot,
+              int64_t *counts, int32_t *flag, int32_t staging_base,
+              int32_t n_devices, int8_t *outcome) {
+    // outcome counters: shared-memory tallies, one global add per block
+    __shared__ unsigned int tally[3 * kPlanMaxParts];
+    for (int i = threadIdx.x; i < 3 * st.n_parts; i += blockDim.x) tally[i] = 0;
+    __syncthreads();
+    const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (u < st.n_union) plan_vertex(st, u, e, s, me, req_ver, glob_ver, halo_row, stage_src,
+                                    stage_row, stage_dst, gw_slot, tally, flag, staging_base,
+                                    n_devices, outcome);
+    __syncthreads();
+    for (int i = threadIdx.x; i < 3 * st.n_parts; i += blockDim.x)
+        if (tally[i]) atomicAdd(reinterpret_cast<unsigned long long *>(counts + i),
+                                (unsigned long long)tally[i]);
+}
+
 inline int grid_for(int64_t work, int threads, int max_blocks = 148 * 16) {
     int64_t b = (work + threads - 1) / threads;
     if (b < 1) b = 1;
@@ -392,7 +465,7 @@ int cg_copy_rows(int64_t n, int F, const int32_t *src_id, const int32_t *src_row
                  float *dst, int64_t ld_dst, void *stream) {
     if (n == 0) return 0;
     const int threads = 256;
-    int blocks = grid_for(n * 32, threads, 148 * 32);
+    int blocks = grid_for(n, threads, 148 * 32);
     bool vec = (F % 4 == 0) && (ld_dst % 4 == 0) && ((uintptr_t)dst % 16 == 0);
     // source alignment is validated on the host side (tab_ld % 4 == 0, 16-B bases)
     if (vec)
@@ -449,12 +522,11 @@ int cg_scale_rows(float *X, int64_t ld, int64_t n_rows, int F, const float *scal
 
 int cg_colsum(int64_t M, int N, const float *D, int64_t ldd, float *db, float *ws, void *stream) {
     if (M == 0 || N == 0) return 0;
-    const int64_t chunk = 2048;
-    int64_t nch = (M + chunk - 1) / chunk;
-    dim3 grid((N + 127) / 128, (unsigned)nch);
+    int64_t nch = (M + kColChunk - 1) / kColChunk;
+    dim3 grid((N + 31) / 32, (unsigned)nch);
     cudaStream_t st = (cudaStream_t)stream;
-    k_colsum_partial<<<grid, 128, 0, st>>>(M, N, D, ldd, chunk, ws);
-    k_reduce_chunks<<<(N + 255) / 256, 256, 0, st>>>(N, nch, ws, db, 0);
+    k_colsum_partial<<<grid, 256, 0, st>>>(M, N, D, ldd, ws);
+    k_reduce_chunks_tree<<<(N + 31) / 32, 256, 0, st>>>(N, nch, ws, db);
     CG_CHECK_LAUNCH("cg_colsum");
     return 2;
 }
@@ -487,6 +559,10 @@ int cg_plan_frozen(const cg_plan_static *st, int epoch, int staleness, int me, i
                    int32_t *stage_dst, int32_t *gw_slot, int64_t *counts, int32_t *flag,
                    int32_t staging_base, int32_t n_devices, int8_t *outcome, void *stream) {
     if (st->n_union == 0) return 0;
+    if (st->n_parts > kPlanMaxParts) {
+        cg_set_error("cg_plan_frozen: too many partition slots");
+        return -1;
+    }
     k_plan_frozen<<<(unsigned)((st->n_union + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
         *st, epoch, staleness, me, req_ver, glob_ver, halo_row, stage_src, stage_row, stage_dst,
         gw_slot, counts, flag, staging_base, n_devices, outcome);

@@ -49,7 +49,11 @@ class Engine:
         self.me = me
         self.D = layout.devices[me]
         self.kind = kind
-        self.dims = list(dims)
+        # the class dimension is padded to a multiple of 4 (16-byte rows for
+        # TMA); padded logit columns have zero weights and zero gradients
+        self.C = int(dims[-1])
+        self.C4 = (self.C + 3) // 4 * 4
+        self.dims = list(dims[:-1]) + [self.C4]
         self.nL = len(dims) - 1
         self.bpe_f = bpe // 4
         self.comm = comm or SoloComm()
@@ -71,9 +75,9 @@ class Engine:
         D, dev, f32, i32, i64 = self.D, self.dev, torch.float32, torch.int32, torch.int64
         dims = self.dims
         self.F = dims[:-1]
-        self.C = dims[-1]
         self.X = [torch.zeros(D.n_rows, F, dtype=f32, device=dev) for F in self.F]
-        self.logits = torch.zeros(D.n_in, self.C, dtype=f32, device=dev)
+        self.logits = torch.zeros(D.n_in, self.C4, dtype=f32, device=dev)
+        self.dL = torch.zeros(D.n_in, self.C4, dtype=f32, device=dev)  # logits gradient
         self.Z = [torch.zeros(D.n_in, F, dtype=f32, device=dev) for F in self.F]
         wmax = max(dims[1:])
         self.dY = [torch.zeros(D.n_in, wmax, dtype=f32, device=dev) for _ in range(2)]
@@ -89,11 +93,20 @@ class Engine:
                 self.pshapes += [(fi, fo), (fo,)]
             else:
                 self.pshapes += [(fi, fo), (fi, fo), (fo,)]
+        # every tensor starts on a 16-byte boundary (TMA / tcgen05 operands)
         sizes = [int(np.prod(s)) for s in self.pshapes]
-        self.poff = np.concatenate(([0], np.cumsum(sizes))).astype(np.int64)
+        padded = [(sz + 3) // 4 * 4 for sz in sizes]
+        self.poff = np.concatenate(([0], np.cumsum(padded))).astype(np.int64)
         self.n_params = int(self.poff[-1])
-        flat = np.concatenate([np.asarray(p, np.float32).ravel() for p in params_init])
-        assert flat.size == self.n_params
+        flat = np.zeros(self.n_params, np.float32)
+        for i, p in enumerate(params_init):
+            p = np.asarray(p, np.float32)
+            if p.shape != tuple(self.pshapes[i]):   # last layer: pad class columns
+                q = np.zeros(self.pshapes[i], np.float32)
+                q[tuple(slice(0, k) for k in p.shape)] = p
+                p = q
+            flat[self.poff[i]:self.poff[i] + sizes[i]] = p.ravel()
+        self.psizes = sizes
         self.params = _dev(flat, f32, dev)
         self.grads = torch.zeros(self.n_params + 1, dtype=f32, device=dev)
         self.adam_m = torch.zeros(self.n_params, dtype=f32, device=dev)
@@ -101,7 +114,7 @@ class Engine:
         ws = 1
         for l in range(self.nL):
             ws = max(ws, call("cg_wgrad_workspace", D.n_in, dims[l], dims[l + 1]),
-                     call("cg_wgrad_workspace", D.n_in, 1, dims[l + 1]))
+                     (D.n_in + 255) // 256 * dims[l + 1])  # cg_colsum: 256-row chunks
         self.ws = torch.zeros(ws, dtype=f32, device=dev)
         self.ce_ws = torch.zeros(max(D.n_in, 1), dtype=f32, device=dev)
         # graph structure
@@ -164,7 +177,12 @@ class Engine:
 
     def param_views(self) -> list[np.ndarray]:
         flat = self.params.detach().cpu().numpy()
-        return [flat[self.poff[i]:self.poff[i + 1]].reshape(s) for i, s in enumerate(self.pshapes)]
+        out = [flat[self.poff[i]:self.poff[i] + self.psizes[i]].reshape(s)
+               for i, s in enumerate(self.pshapes)]
+        per = 2 if self.kind == "gcn" else 3
+        for i in range(len(out) - per, len(out)):  # strip the class padding
+            out[i] = out[i][..., :self.C].copy()
+        return out
 
     def _p(self, i: int) -> int:
         return ptr(self.params) + 4 * int(self.poff[i])
@@ -377,15 +395,14 @@ class Engine:
                      0 if last else 1, None, ptr(out), Fo, self.gemm_mode, st)
         # ---------------- loss
         n_total = self.L.n
-        dY = self.dY[0]
         loss_ptr = ptr(self.grads) + 4 * self.n_params
-        call("cg_softmax_ce", n_in, self.C, ptr(self.logits), self.C, ptr(self.labels),
-             1.0 / n_total, ptr(dY), self.C, loss_ptr, ptr(self.ce_ws), st)
+        call("cg_softmax_ce", n_in, self.C, ptr(self.logits), self.C4, ptr(self.labels),
+             1.0 / n_total, ptr(self.dL), self.C4, loss_ptr, ptr(self.ce_ws), st)
         # ---------------- backward
         cur = 0
         for l in range(nL - 1, -1, -1):
             F, Fo = self.F[l], self.dims[l + 1]
-            dY = self.dY[cur]
+            dY = self.dL if l == nL - 1 else self.dY[cur]
             if kind == "gcn":
                 call("cg_wgrad", n_in, F, Fo, ptr(self.Z[l]), F, ptr(dY), Fo, self._g(2 * l),
                      ptr(self.ws), self.gemm_mode, st)
@@ -398,7 +415,7 @@ class Engine:
                 call("cg_colsum", n_in, Fo, ptr(dY), Fo, self._g(3 * l + 2), ptr(self.ws), st)
             if l == 0:
                 break
-            nxt = self.dY[1 - cur]
+            nxt = self.dY[1 - cur] if l != nL - 1 else self.dY[cur]
             if kind == "gcn":
                 call("cg_gemm", n_in, F, Fo, ptr(dY), Fo, self._p(2 * l), 0, None, 0, None, 1,
                      None, 0, ptr(self.norm_dst), ptr(self.G), F, self.gemm_mode, st)
@@ -420,7 +437,8 @@ class Engine:
             if timers:
                 b.record()
                 bwd_ev.append((a, b))
-            cur = 1 - cur
+            if l != nL - 1:
+                cur = 1 - cur
         # ---------------- K7 + optimizer
         self.comm.allreduce_(self.grads)
         self._gw(nL - 1)
@@ -477,7 +495,7 @@ class Engine:
 
     def logits_global(self) -> np.ndarray:
         """This device's logits keyed by vertex id: (verts, logits)."""
-        return self.D.verts, self.logits.detach().cpu().numpy()
+        return self.D.verts, self.logits[:, :self.C].detach().cpu().numpy()
 
     def close(self):
         self.comm.close()

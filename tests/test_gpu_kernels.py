@@ -178,3 +178,60 @@ def test_hash_inputs_bit_exact_vs_oracle():
     _sync()
     assert np.array_equal(X.cpu().numpy(), omp.features(n, F, 0))
     assert np.array_equal(y.cpu().numpy(), omp.labels(n, Cc, 1))
+
+
+TC_SHAPES = [  # M, N, K1, K2, trans_b
+    (1000, 40, 256, 0, 0), (777, 256, 128, 0, 0), (513, 64, 36, 0, 1), (2048, 256, 256, 0, 1),
+    (300, 128, 64, 64, 0), (4099, 48, 40, 0, 1), (128, 16, 32, 0, 0), (1536, 256, 256, 256, 0)]
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("shape", TC_SHAPES, ids=lambda s: "x".join(map(str, s)))
+def test_gemm_tcgen05(shape, mode):
+    """tcgen05 kind::tf32 GEMM: 3xTF32 (mode 1) ~fp32, 1xTF32 (mode 2) ~1e-3."""
+    import torch
+    from paper_2508_13716_b200._lib import call, ptr
+    M, N, K1, K2, tb = shape
+    rng = np.random.default_rng(M + N)
+    A = rng.standard_normal((M, K1)).astype(np.float32)
+    B = rng.standard_normal((N, K1) if tb else (K1, N)).astype(np.float32)
+    A2 = rng.standard_normal((M, K2)).astype(np.float32) if K2 else None
+    B2 = (rng.standard_normal((N, K2) if tb else (K2, N)).astype(np.float32)) if K2 else None
+    bias = rng.standard_normal(N).astype(np.float32)
+    rs = rng.random(M).astype(np.float32)
+    ref = A.astype(np.float64) @ (B.T if tb else B)
+    if K2:
+        ref += A2.astype(np.float64) @ (B2.T if tb else B2)
+    ref = np.maximum(ref + bias, 0) * rs[:, None]
+    out = torch.full((M, N), float("nan"), device="cuda")
+    k = [_t(A), _t(B), _t(A2) if K2 else None, _t(B2) if K2 else None, _t(bias), _t(rs)]
+    call("cg_gemm", M, N, K1, ptr(k[0]), K1, ptr(k[1]), K2, ptr(k[2]), K2, ptr(k[3]), tb,
+         ptr(k[4]), 1, ptr(k[5]), ptr(out), N, mode, _st())
+    _sync()
+    got = out.cpu().numpy()
+    scale = np.abs(ref).max()
+    err = np.abs(got - ref).max() / scale
+    assert err < (1e-5 if mode == 1 else 2e-3), err
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("MKN", [(10000, 128, 40), (169343 // 8, 256, 256), (5000, 256, 128), (169343, 256, 256)])
+def test_wgrad_tcgen05(MKN, mode):
+    import torch
+    from paper_2508_13716_b200._lib import call, ptr
+    M, K, N = MKN
+    rng = np.random.default_rng(K + N)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    D = rng.standard_normal((M, N)).astype(np.float32)
+    ws = torch.zeros(call("cg_wgrad_workspace", M, K, N), device="cuda")
+    dW = torch.zeros(K, N, device="cuda")
+    tA, tD = _t(A), _t(D)
+    call("cg_wgrad", M, K, N, ptr(tA), K, ptr(tD), N, ptr(dW), ptr(ws), mode, _st())
+    _sync()
+    ref = A.T.astype(np.float64) @ D
+    err = np.abs(dW.cpu().numpy() - ref).max() / np.abs(ref).max()
+    assert err < (1e-5 if mode == 1 else 2e-3), err
+    first = dW.clone()
+    call("cg_wgrad", M, K, N, ptr(tA), K, ptr(tD), N, ptr(dW), ptr(ws), mode, _st())
+    _sync()
+    assert torch.equal(first, dW)  # deterministic split-K

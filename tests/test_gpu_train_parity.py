@@ -59,6 +59,21 @@ def test_train_matches_oracle(case):
         assert rel_err(rep.logits_per_epoch[e], o.logits) <= TOL, e
 
 
+@pytest.mark.parametrize("kind", ["gcn", "sage"])
+def test_train_3xtf32_tensor_core_parity(kind):
+    """Same contract with the tcgen05 3xTF32 GEMMs (the bench's default)."""
+    from paper_2508_13716_b200 import hostgraph as H
+    g, ps, og, ops = workload(700, 6.0, 4)
+    f_dim, C = (32, 64, 64), 10
+    caps = H.uniform_capacities(ps, 150, f_dim)
+    cfg = H.SimConfig(epochs=4, policy="jaca", staleness_bound=1, f_dim=f_dim, L=3)
+    rep = _train(g, ps, caps, cfg, kind, C, gemm="3xtf32")
+    _, outs, _ = oracle_run(og, ops, kind, f_dim, C, caps, "jaca", 1, 4)
+    for e, o in enumerate(outs):
+        assert abs(rep.losses[e] - o.loss) <= TOL * abs(o.loss)
+        assert rel_err(rep.logits_per_epoch[e], o.logits) <= TOL, e
+
+
 def test_gpu_planner_handoff_matches_host_planner():
     """K6 (GPU frozen plan) vs the exact host planner on every epoch."""
     from paper_2508_13716_b200 import hostgraph as H
