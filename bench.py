@@ -180,7 +180,9 @@ def run_ours(args):
     fwd_ms = np.array([s.spmm_fwd_ms for s in stats])  # (K, L)
     bwd_ms = np.array([s.spmm_bwd_ms for s in stats])  # (K, L-1)
     fb = [spmm_bytes(D.nnz_fwd, D.n_in, F, D.n_halo) for F in F_DIM]
-    bb = [spmm_bytes(D.nnz_bwd, D.n_in, F, 0) for F in reversed(F_DIM[1:])]
+    widths = list(F_DIM) + [eng.C4]   # backward aggregates min(F_in, F_out) wide
+    bb = [spmm_bytes(D.nnz_bwd, D.n_in, min(widths[l], widths[l + 1]), 0)
+          for l in range(len(F_DIM) - 1, 0, -1)]
     tot_bytes = args.steps * (sum(fb) + sum(bb))
     tot_ms = float(fwd_ms.sum() + bwd_ms.sum())
     achieved = tot_bytes / (tot_ms / 1e3) / 1e9

@@ -62,6 +62,9 @@ int cg_hash_labels(int32_t *out, const int32_t *vertex, int64_t n_rows, int C,
 /* X[r*ld + k] *= scale[r] (GCN source-degree pre-scaling of uploaded rows). */
 int cg_scale_rows(float *X, int64_t ld, int64_t n_rows, int F, const float *scale,
                   void *stream);
+/* dst[r*ldd + k] = src[r*lds + k] * scale[r]. */
+int cg_scale_rows_to(float *dst, int64_t ldd, const float *src, int64_t lds, int64_t n_rows,
+                     int F, const float *scale, void *stream);
 
 /* ---- K3: halo staging / cache write-through ---------------------------- */
 /* For i in [0, n): if src_id[i] >= 0 and dst_row[i] >= 0:
@@ -90,12 +93,13 @@ int cg_spmm(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col,
 /* ---- K5: dense transform ---------------------------------------------- */
 /* C[m, n] = epi( sum_k A1[m,k] B1[k,n] + sum_k A2[m,k] B2[k,n] )  (A2 optional)
  * trans_b = 1 means B is supplied as [N x K] row-major (use B^T).
- * epi: (+ bias[n]) -> (relu if relu) -> (* row_scale[m]).
+ * epi: (+ bias[n]) -> (relu if relu) -> (* row_scale[m])
+ *      -> (* (mask[m*ldm + n] > 0)) when mask != NULL (ReLU backward).
  * mode: 0 = fp32 SIMT, 1 = 3xTF32 tcgen05 (parity), 2 = 1xTF32 tcgen05.   */
 int cg_gemm(int64_t M, int N, int K1, const float *A1, int64_t lda1,
             const float *B1, int K2, const float *A2, int64_t lda2, const float *B2,
             int trans_b, const float *bias, int relu, const float *row_scale,
-            float *C, int64_t ldc, int mode, void *stream);
+            const float *mask, int64_t ldm, float *C, int64_t ldc, int mode, void *stream);
 /* dW[k, n] (+)= sum_m A[m, k] * D[m, n]; deterministic split over m.
  * ws must hold cg_wgrad_workspace(M, K, N) floats.                        */
 int64_t cg_wgrad_workspace(int64_t M, int K, int N);

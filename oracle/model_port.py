@@ -200,8 +200,16 @@ class Trainer:
         self.y = y
         self.e = 0
 
-    def step(self, versions_e) -> EpochOut:
-        """versions_e[p]: served versions of partition p's halo (ascending id)."""
+    def step(self, versions_e, forced_params=None) -> EpochOut:
+        """versions_e[p]: served versions of partition p's halo (ascending id).
+
+        forced_params: run this epoch from these weights instead of the
+        oracle's own trajectory (isolates one epoch's arithmetic from Adam's
+        amplification of earlier rounding differences).
+        """
+        if forced_params is not None:
+            for dst, src in zip(self.params, forced_params):
+                dst[...] = np.asarray(src, np.float64)
         spec, params, L, P, n = self.spec, self.params, self.L, self.P, self.g.n
         inner, halo, ops, history = self.inner, self.halo, self.ops, self.history
         self.e += 1

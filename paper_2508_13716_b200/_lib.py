@@ -47,9 +47,10 @@ SIGNATURES = {
     "cg_hash_features": [P, I64, P, I64, INT, U32, P, P],
     "cg_hash_labels": [P, P, I64, INT, U32, P],
     "cg_scale_rows": [P, I64, I64, INT, P, P],
+    "cg_scale_rows_to": [P, I64, P, I64, I64, INT, P, P],
     "cg_copy_rows": [I64, INT, P, P, P, P, P, P, I64, P],
     "cg_spmm": [I64, INT, P, P, I64, P, P, I64, P, P, I64, P, I64, P, I64, P],
-    "cg_gemm": [I64, INT, INT, P, I64, P, INT, P, I64, P, INT, P, INT, P, P, I64, INT, P],
+    "cg_gemm": [I64, INT, INT, P, I64, P, INT, P, I64, P, INT, P, INT, P, P, I64, P, I64, INT, P],
     "cg_wgrad_workspace": [I64, INT, INT],
     "cg_wgrad": [I64, INT, INT, P, I64, P, I64, P, P, INT, P],
     "cg_colsum": [I64, INT, P, I64, P, P, P],
@@ -109,7 +110,8 @@ def lib():
 
 # device entry points report how many kernels they launched; the running
 # total is the bench's "gpu_launches" evidence
-KERNEL_ENTRY = {"cg_hash_features", "cg_hash_labels", "cg_scale_rows", "cg_copy_rows",
+KERNEL_ENTRY = {"cg_hash_features", "cg_hash_labels", "cg_scale_rows", "cg_scale_rows_to",
+                "cg_copy_rows",
                 "cg_spmm", "cg_gemm", "cg_wgrad", "cg_colsum", "cg_softmax_ce", "cg_adam",
                 "cg_plan_frozen"}
 launches = {"total": 0}

@@ -65,6 +65,7 @@ class TrainReport:
     logits: np.ndarray | None = field(default=None, repr=False, compare=False)
     logits_per_epoch: list | None = field(default=None, repr=False, compare=False)
     params: list | None = field(default=None, repr=False, compare=False)
+    params_per_epoch: list | None = field(default=None, repr=False, compare=False)
     n_edges: int = 0
     n_layers: int = 0
     n_devices: int = 1
@@ -139,8 +140,8 @@ def _model_times(ps, sigma, nrm, cfg):
 
 def train(g, part, profiles, caps, cfg, record_trace: bool = False, *, model: str = "gcn",
           num_classes: int = 40, gemm: str = "fp32", plan_mode: str = "auto",
-          keep_logits: str = "last", timers: bool = True, seed: int = 2,
-          on_epoch=None) -> TrainReport:
+          keep_logits: str = "last", keep_params: bool = False, timers: bool = True,
+          seed: int = 2, on_epoch=None) -> TrainReport:
     """Run cfg.epochs real training epochs of the partitioned GNN on B200s.
 
     One partition slot per GPU when torch.distributed is initialised with
@@ -198,9 +199,13 @@ def train(g, part, profiles, caps, cfg, record_trace: bool = False, *, model: st
                       n_layers=len(cfg.f_dim), n_devices=world)
     if keep_logits == "all":
         rep.logits_per_epoch = []
+    if keep_params:
+        rep.params_per_epoch = []   # weights at the START of each epoch
     tot = np.zeros(3, np.int64)
     try:
         for e in range(1, cfg.epochs + 1):
+            if keep_params:
+                rep.params_per_epoch.append(eng.param_views())
             stt = eng.run_epoch(e, timers=timers)
             rep.losses.append(stt.loss)
             rep.epoch_seconds.append(stt.seconds)

@@ -19,8 +19,8 @@ extern void cg_set_error(const std::string &msg);
 extern int cg_cuda_fail(cudaError_t e, const char *what);
 int cg_gemm_tc(int64_t M, int N, int K1, const float *A1, int64_t lda1, const float *B1, int K2,
                const float *A2, int64_t lda2, const float *B2, int trans_b, const float *bias,
-               int relu, const float *row_scale, float *C, int64_t ldc, int mode,
-               cudaStream_t st);
+               int relu, const float *row_scale, const float *mask, int64_t ldm, float *C,
+               int64_t ldc, int mode, cudaStream_t st);
 int cg_wgrad_tc(int64_t M, int K, int N, const float *A, int64_t lda, const float *D, int64_t ldd,
                 float *ws, int64_t chunk, int64_t n_chunks, int mode, cudaStream_t st);
 
@@ -38,7 +38,8 @@ __global__ void __launch_bounds__(NT)
 k_gemm(int64_t M, int N, int K1, const float *__restrict__ A1, int64_t lda1,
        const float *__restrict__ B1, int K2, const float *__restrict__ A2, int64_t lda2,
        const float *__restrict__ B2, int trans_b, const float *__restrict__ bias, int relu,
-       const float *__restrict__ row_scale, float *__restrict__ C, int64_t ldc) {
+       const float *__restrict__ row_scale, const float *__restrict__ mask, int64_t ldm,
+       float *__restrict__ C, int64_t ldc) {
     __shared__ float As[BK][BM + 4];
     __shared__ float Bs[BK][BN];
     const int tid = threadIdx.x;
@@ -102,7 +103,9 @@ k_gemm(int64_t M, int N, int K1, const float *__restrict__ A1, int64_t lda1,
             float v = acc[i][j];
             if (bias) v += bias[n];
             if (relu) v = fmaxf(v, 0.f);
-            C[m * ldc + n] = v * rs;
+            v *= rs;
+            if (mask && !(mask[m * ldm + n] > 0.f)) v = 0.f;
+            C[m * ldc + n] = v;
         }
     }
 }
@@ -160,9 +163,17 @@ __global__ void k_wgrad_reduce(int64_t n_out, int64_t n_chunks, const float *__r
                                float *__restrict__ out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n_out) return;
-    float s = 0.f;
-    for (int64_t c = 0; c < n_chunks; ++c) s += ws[c * n_out + i];
-    out[i] = s;
+    // four independent chains (pipelined loads), combined in a fixed order
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    int64_t c = 0;
+    for (; c + 3 < n_chunks; c += 4) {
+        s0 += ws[c * n_out + i];
+        s1 += ws[(c + 1) * n_out + i];
+        s2 += ws[(c + 2) * n_out + i];
+        s3 += ws[(c + 3) * n_out + i];
+    }
+    for (; c < n_chunks; ++c) s0 += ws[c * n_out + i];
+    out[i] = (s0 + s1) + (s2 + s3);
 }
 
 constexpr int64_t kWgradChunk = 1024;  // short TC accumulation chains (accuracy), many CTAs
@@ -173,14 +184,16 @@ extern "C" {
 
 int cg_gemm(int64_t M, int N, int K1, const float *A1, int64_t lda1, const float *B1, int K2,
             const float *A2, int64_t lda2, const float *B2, int trans_b, const float *bias,
-            int relu, const float *row_scale, float *C, int64_t ldc, int mode, void *stream) {
+            int relu, const float *row_scale, const float *mask, int64_t ldm, float *C,
+            int64_t ldc, int mode, void *stream) {
     if (M == 0 || N == 0) return 0;
     if (mode != 0)
         return cg_gemm_tc(M, N, K1, A1, lda1, B1, K2, A2, lda2, B2, trans_b, bias, relu,
-                          row_scale, C, ldc, mode, (cudaStream_t)stream);
+                          row_scale, mask, ldm, C, ldc, mode, (cudaStream_t)stream);
     dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN));
     k_gemm<<<grid, NT, 0, (cudaStream_t)stream>>>(M, N, K1, A1, lda1, B1, K2, A2, lda2, B2,
-                                                 trans_b, bias, relu, row_scale, C, ldc);
+                                                 trans_b, bias, relu, row_scale, mask, ldm,
+                                                 C, ldc);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 1 : cg_cuda_fail(e, "k_gemm");
 }

@@ -37,10 +37,13 @@ namespace tc {
 constexpr int BM = 128;          // UMMA M (cta_group::1)
 constexpr int BK = 32;           // fp32 elements per 128-byte swizzle row
 constexpr int UK = 8;            // K per tcgen05.mma kind::tf32
-constexpr int BN_MAX = 128;
-constexpr int TILE_BYTES = BM * BK * 4;          // 16 KB, A or B operand stage
-constexpr int STAGE_BYTES_1X = 2 * TILE_BYTES;   // A + B
-constexpr int STAGE_BYTES_3X = 4 * TILE_BYTES;   // A, B, A_lo, B_lo
+constexpr int BN_MAX = 256;
+constexpr int A_BYTES = BM * BK * 4;             // 16 KB A operand stage
+constexpr int B_BYTES = BN_MAX * BK * 4;         // 32 KB B operand stage
+constexpr int HI_BYTES = A_BYTES + B_BYTES;      // [A | B]
+constexpr int STAGE_BYTES_1X = HI_BYTES;         // A, B
+constexpr int STAGE_BYTES_3X = 2 * HI_BYTES;     // A, B, A_lo, B_lo (lo = hi + HI_BYTES)
+constexpr int EPI_BYTES = 4 * 32 * 33 * 4;  // epilogue transpose staging
 constexpr int THREADS = 384;  // 12 warps: TMA, MMA, -, -, 4 epilogue, 4 splitter
 
 struct Op {
@@ -57,6 +60,8 @@ struct Params {
     const float *bias;
     int relu;
     const float *row_scale;
+    const float *mask;
+    int64_t ldm;
     float *C;
     int64_t ldc;
     int split3;      // 3xTF32
@@ -191,9 +196,10 @@ __global__ void __launch_bounds__(THREADS, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mB0,
           const __grid_constant__ CUtensorMap mA1, const __grid_constant__ CUtensorMap mB1,
           const Params p) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // no static shared memory in this kernel, so the dynamic window starts
+    // 1024-byte aligned (required by the 128B-swizzle atoms); pointers stay
+    // derived from the __shared__ array so accesses compile to LDS/STS
+    extern __shared__ __align__(1024) uint8_t smem[];
     const int S = p.stages;
     const int stage_bytes = p.split3 ? STAGE_BYTES_3X : STAGE_BYTES_1X;
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + S * stage_bytes);
@@ -202,6 +208,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
     uint64_t *tfull = empty + S;   // [2] accumulator ready
     uint64_t *tempty = tfull + 2;  // [2] accumulator drained
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    float *epi_stage = reinterpret_cast<float *>(smem + S * stage_bytes + 1024);  // 4 x 32x33
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int n_tiles = (p.N + p.BN - 1) / p.BN;
@@ -224,7 +231,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
-                     "r"(256));
+                     "r"(512));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -249,8 +256,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                     mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
                     const int k0 = kb * BK;
                     uint8_t *sa = smem + s * stage_bytes;
-                    uint8_t *sb = sa + TILE_BYTES;
-                    mbar_expect_tx(&full[s], TILE_BYTES + bbytes);
+                    uint8_t *sb = sa + A_BYTES;
+                    mbar_expect_tx(&full[s], A_BYTES + bbytes);
                     if (p.op[o].a_mn) {
                         for (int b = 0; b < 4; ++b)
                             tma_load_2d(ma, &full[s], sa + b * 4096, (int)(tc.m0 + 32 * b), k0);
@@ -274,7 +281,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
             const uint32_t acc_buf = ti & 1;
             mbar_wait(&tempty[acc_buf], ((ti >> 1) & 1) ^ 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t tmem_d = tmem_base + acc_buf * 128;
+            const uint32_t tmem_d = tmem_base + acc_buf * BN_MAX;
             bool first = true;
             for (int o = 0; o < p.n_ops; ++o) {
                 int kb0, nkb;
@@ -296,8 +303,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                     else mbar_wait(&full[s], ph);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     const uint32_t sa = smem_u32(smem + s * stage_bytes);
-                    const uint32_t sb = sa + TILE_BYTES;
-                    const uint32_t sa_lo = sa + 2 * TILE_BYTES, sb_lo = sa + 3 * TILE_BYTES;
+                    const uint32_t sb = sa + A_BYTES;
+                    const uint32_t sa_lo = sa + HI_BYTES, sb_lo = sb + HI_BYTES;
 #pragma unroll
                     for (int j = 0; j < BK / UK; ++j) {
                         const uint64_t da = smem_desc(sa + j * a_step, a_lbo, a_sbo, a_lay);
@@ -321,42 +328,48 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
         }
     } else if (warp >= 4 && warp < 8) {
         // ------------------------------------------------ epilogue
+        // Warp q owns TMEM lanes (= tile rows) 32q..32q+31.  Each 32x32
+        // sub-tile goes TMEM -> registers (thread = row) -> padded smem ->
+        // registers (lane = column), so bias / mask loads and the output
+        // stores are 128-byte coalesced row segments.
         const int q = warp & 3;
+        float (*stg)[33] = reinterpret_cast<float (*)[33]>(epi_stage + q * 32 * 33);
         uint32_t ti = 0;
         for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++ti) {
             const TileCoord tc = tile_of(p, t, n_tiles, m_tiles);
             const uint32_t acc_buf = ti & 1;
             mbar_wait(&tfull[acc_buf], (ti >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const int64_t row = tc.m0 + 32 * q + lane;
-            const bool live = row < p.M;
-            const float rs = (p.row_scale && live) ? p.row_scale[row] : 1.f;
-            float *crow = p.k_chunk > 0 ? p.C + ((int64_t)tc.z * p.M + row) * p.ldc
-                                        : p.C + row * p.ldc;
-            const bool vec = ((p.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0);
+            const int64_t row0 = tc.m0 + 32 * q;
+            float *cbase = p.k_chunk > 0 ? p.C + (int64_t)tc.z * p.M * p.ldc : p.C;
+            const float rs_lane =
+                (p.row_scale && row0 + lane < p.M) ? p.row_scale[row0 + lane] : 1.f;
             for (int c0 = 0; c0 < p.BN; c0 += 32) {
-                float v[32];
-                tmem_ld32(tmem_base + acc_buf * 128 + ((uint32_t)(32 * q) << 16) + c0, v);
-                if (!live) continue;
+                const int n = tc.n0 + c0 + lane;
+                const bool col_ok = n < p.N && c0 + lane < p.BN;
+                // issue the global loads first so they overlap the TMEM read
+                float mk[32];
+                if (p.mask) {
 #pragma unroll
-                for (int i = 0; i < 32; i += 4) {
-                    const int n = tc.n0 + c0 + i;
-                    float x[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        float y = v[i + u];
-                        if (p.bias && n + u < p.N) y += p.bias[n + u];
-                        if (p.relu) y = fmaxf(y, 0.f);
-                        x[u] = y * rs;
-                    }
-                    if (vec && n + 3 < p.N && c0 + i + 3 < p.BN) {
-                        *reinterpret_cast<float4 *>(crow + n) = make_float4(x[0], x[1], x[2], x[3]);
-                    } else {
-#pragma unroll
-                        for (int u = 0; u < 4; ++u)
-                            if (n + u < p.N && c0 + i + u < p.BN) crow[n + u] = x[u];
-                    }
+                    for (int r = 0; r < 32; ++r)
+                        mk[r] = (col_ok && row0 + r < p.M) ? p.mask[(row0 + r) * p.ldm + n] : 1.f;
                 }
+                const float bias = (p.bias && col_ok) ? p.bias[n] : 0.f;
+                float v[32];
+                tmem_ld32(tmem_base + acc_buf * BN_MAX + ((uint32_t)(32 * q) << 16) + c0, v);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) stg[lane][i] = v[i];
+                __syncwarp();
+#pragma unroll
+                for (int r = 0; r < 32; ++r) {
+                    const int64_t row = row0 + r;
+                    float y = stg[r][lane] + bias;
+                    if (p.relu) y = fmaxf(y, 0.f);
+                    y *= __shfl_sync(0xffffffffu, rs_lane, r);
+                    if (p.mask && !(mk[r] > 0.f)) y = 0.f;
+                    if (col_ok && row < p.M) cbase[row * p.ldc + n] = y;
+                }
+                __syncwarp();
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             mbar_arrive(&tempty[acc_buf]);
@@ -374,9 +387,11 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                     const int s = it % S;
                     mbar_wait(&full[s], (it / S) & 1);
                     uint4 *hi = reinterpret_cast<uint4 *>(smem + s * stage_bytes);
-                    uint4 *lo = reinterpret_cast<uint4 *>(smem + s * stage_bytes + 2 * TILE_BYTES);
+                    uint4 *lo = reinterpret_cast<uint4 *>(smem + s * stage_bytes + HI_BYTES);
+                    const int n16 =
+                        (A_BYTES + (p.op[o].b_mn ? nb_b * 32 * BK * 4 : p.BN * BK * 4)) / 16;
 #pragma unroll 4
-                    for (int i = t128; i < 2 * TILE_BYTES / 16; i += 128) {
+                    for (int i = t128; i < n16; i += 128) {
                         uint4 w = hi[i];
                         uint4 h = make_uint4(w.x & 0xFFFFE000u, w.y & 0xFFFFE000u,
                                              w.z & 0xFFFFE000u, w.w & 0xFFFFE000u);
@@ -399,7 +414,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                     "r"(256));
+                     "r"(512));
     }
 }
 
@@ -443,12 +458,12 @@ int launch(const Params &p0, const CUtensorMap &a0, const CUtensorMap &b0, const
            const CUtensorMap &b1, int grid_z, cudaStream_t st) {
     Params p = p0;
     const int stage_bytes = p.split3 ? STAGE_BYTES_3X : STAGE_BYTES_1X;
-    p.stages = p.split3 ? 3 : 6;
-    const size_t smem = (size_t)p.stages * stage_bytes + 1024 + 512;
+    p.stages = p.split3 ? 2 : 4;
+    const size_t smem = (size_t)p.stages * stage_bytes + 1024 + 1024 + EPI_BYTES;
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)(6 * STAGE_BYTES_1X + 1024 + 512));
+                                             (int)(4 * STAGE_BYTES_1X + 1024 + 1024 + EPI_BYTES));
         if (e != cudaSuccess) return cg_cuda_fail(e, "cudaFuncSetAttribute(k_gemm_tc)");
         attr_set = true;
     }
@@ -477,8 +492,8 @@ inline int bn_for(int N) {
 // row-major (MN-major, trans_b = 0) or [N x K] row-major (K-major, trans_b = 1).
 int cg_gemm_tc(int64_t M, int N, int K1, const float *A1, int64_t lda1, const float *B1, int K2,
                const float *A2, int64_t lda2, const float *B2, int trans_b, const float *bias,
-               int relu, const float *row_scale, float *C, int64_t ldc, int mode,
-               cudaStream_t st) {
+               int relu, const float *row_scale, const float *mask, int64_t ldm, float *C,
+               int64_t ldc, int mode, cudaStream_t st) {
     using namespace tc;
     if (mode != 1 && mode != 2) {
         cg_set_error("cg_gemm: unknown mode");
@@ -497,6 +512,8 @@ int cg_gemm_tc(int64_t M, int N, int K1, const float *A1, int64_t lda1, const fl
     p.bias = bias;
     p.relu = relu;
     p.row_scale = row_scale;
+    p.mask = mask;
+    p.ldm = ldm;
     p.C = C;
     p.ldc = ldc;
     p.k_chunk = 0;

@@ -207,29 +207,39 @@ k_spmm(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
 
 // ---------------------------------------------------------------- K8 ------
 
-__global__ void k_softmax_ce(int64_t n, int C, const float *__restrict__ logits, int64_t ld,
-                             const int32_t *__restrict__ label, float inv_n,
-                             float *__restrict__ grad, int64_t ldg, float *__restrict__ row_loss) {
-    const int lane = threadIdx.x & 31;
-    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
-    int64_t nw = (int64_t)gridDim.x * blockDim.x / 32;
-    for (int64_t r = warp; r < n; r += nw) {
+__global__ void __launch_bounds__(256)
+k_softmax_ce(int64_t n, int C, const float *__restrict__ logits, int64_t ld,
+             const int32_t *__restrict__ label, float inv_n, float *__restrict__ grad,
+             int64_t ldg, float *__restrict__ block_loss) {
+    // one warp per row; per-block loss partials combined in a fixed order
+    __shared__ float wl[8];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    float acc = 0.f;
+    for (int64_t r = blockIdx.x * 8 + w; r < n; r += (int64_t)gridDim.x * 8) {
         const float *z = logits + r * ld;
         float mx = -INFINITY;
         for (int c = lane; c < C; c += 32) mx = fmaxf(mx, z[c]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         float se = 0.f;
-        for (int c = lane; c < C; c += 32) se += expf(z[c] - mx);
+        for (int c = lane; c < C; c += 32) se += __expf(z[c] - mx);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
-        const float lse = logf(se);
+        const float lse = __logf(se);
         const int y = label[r];
         for (int c = lane; c < C; c += 32) {
-            float p = expf(z[c] - mx - lse);
+            float p = __expf(z[c] - mx - lse);
             grad[r * ldg + c] = (p - (c == y ? 1.f : 0.f)) * inv_n;
         }
-        if (lane == 0) row_loss[r] = lse - (z[y] - mx);
+        acc += lse - (z[y] - mx);
+    }
+    if (lane == 0) wl[w] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) t += wl[k];
+        block_loss[blockIdx.x] = t;
     }
 }
 
@@ -250,7 +260,7 @@ __global__ void k_sum_fixed(const float *__restrict__ x, int64_t n, float *__res
 // Column sums over m in fixed chunks of kColChunk rows: lanes own columns
 // (coalesced 128 B rows), the 8 warps of a block take interleaved rows, and
 // the 8 per-warp sums are combined in a fixed order -> ws[chunk][n].
-constexpr int kColChunk = 256;
+constexpr int kColChunk = 2048;
 __global__ void __launch_bounds__(256)
 k_colsum_partial(int64_t M, int N, const float *__restrict__ D, int64_t ldd,
                  float *__restrict__ ws) {
@@ -274,18 +284,27 @@ k_colsum_partial(int64_t M, int N, const float *__restrict__ D, int64_t ldd,
     }
 }
 
-// out[i] = sum_c ws[c][i], fixed order: 8 warps stride the chunks, then a
-// fixed combination of the 8 partials.
+// out[i] = sum_c ws[c][i], fixed order: 8 warps stride the chunks (each
+// keeping 4 independent partial sums so the loads pipeline), then a fixed
+// combination of the partials.
 __global__ void __launch_bounds__(256)
 k_reduce_chunks_tree(int64_t n_out, int64_t n_chunks, const float *__restrict__ ws,
                      float *__restrict__ out) {
     __shared__ float part[8][33];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t i = blockIdx.x * 32 + lane;
-    float s = 0.f;
-    if (i < n_out)
-        for (int64_t c = w; c < n_chunks; c += 8) s += ws[c * n_out + i];
-    part[w][lane] = s;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    if (i < n_out) {
+        int64_t c = w;
+        for (; c + 24 < n_chunks; c += 32) {
+            s0 += ws[c * n_out + i];
+            s1 += ws[(c + 8) * n_out + i];
+            s2 += ws[(c + 16) * n_out + i];
+            s3 += ws[(c + 24) * n_out + i];
+        }
+        for (; c < n_chunks; c += 8) s0 += ws[c * n_out + i];
+    }
+    part[w][lane] = (s0 + s1) + (s2 + s3);
     __syncthreads();
     if (w == 0 && i < n_out) {
         float t = 0.f;
@@ -311,6 +330,17 @@ __global__ void k_scale_rows(float *__restrict__ X, int64_t ld, int64_t n, int F
          i += (int64_t)gridDim.x * blockDim.x) {
         int64_t r = i / F;
         X[r * ld + (i - r * F)] *= scale[r];
+    }
+}
+
+__global__ void k_scale_rows_to(float *__restrict__ dst, int64_t ldd, const float *__restrict__ src,
+                                int64_t lds, int64_t n, int F, const float *__restrict__ scale) {
+    int64_t total = n * (int64_t)F;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = i / F;
+        int64_t c = i - r * F;
+        dst[r * ldd + c] = src[r * lds + c] * scale[r];
     }
 }
 
@@ -520,6 +550,15 @@ int cg_scale_rows(float *X, int64_t ld, int64_t n_rows, int F, const float *scal
     return 1;
 }
 
+int cg_scale_rows_to(float *dst, int64_t ldd, const float *src, int64_t lds, int64_t n_rows,
+                     int F, const float *scale, void *stream) {
+    if (n_rows == 0 || F == 0) return 0;
+    k_scale_rows_to<<<grid_for(n_rows * F, 256), 256, 0, (cudaStream_t)stream>>>(
+        dst, ldd, src, lds, n_rows, F, scale);
+    CG_CHECK_LAUNCH("k_scale_rows_to");
+    return 1;
+}
+
 int cg_colsum(int64_t M, int N, const float *D, int64_t ldd, float *db, float *ws, void *stream) {
     if (M == 0 || N == 0) return 0;
     int64_t nch = (M + kColChunk - 1) / kColChunk;
@@ -536,9 +575,9 @@ int cg_softmax_ce(int64_t n_rows, int C, const float *logits, int64_t ld, const 
                   void *stream) {
     if (n_rows == 0) return 0;
     cudaStream_t st = (cudaStream_t)stream;
-    k_softmax_ce<<<grid_for(n_rows * 32, 256, 148 * 32), 256, 0, st>>>(n_rows, C, logits, ld,
-                                                                      label, inv_n, grad, ldg, ws);
-    k_sum_fixed<<<1, 1024, 0, st>>>(ws, n_rows, loss_out);
+    const int blocks = grid_for(n_rows * 32, 256, 148 * 8);
+    k_softmax_ce<<<blocks, 256, 0, st>>>(n_rows, C, logits, ld, label, inv_n, grad, ldg, ws);
+    k_sum_fixed<<<1, 1024, 0, st>>>(ws, blocks, loss_out);
     CG_CHECK_LAUNCH("cg_softmax_ce");
     return 2;
 }

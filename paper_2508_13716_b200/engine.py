@@ -166,11 +166,20 @@ class Engine:
             self.tab_ld.append(_dev(np.array([F] * nd + [self.bpe_f], np.int64), i64, dev))
         gpeers = self.comm.exchange_pointers(ptr(self.G), self.dev.index)
         self.tabG = _dev(np.array(gpeers, np.uint64).view(np.int64), torch.int64, dev)
-        self.tabG_ld = {F: _dev(np.full(nd, F, np.int64), i64, dev) for F in set(self.F)}
+        self._tabG_lds = {}
+        # aggregated narrow gradients (backward aggregate-then-transform layers)
+        self.T = torch.zeros(D.n_in, max(self.dims[1:]), dtype=f32, device=dev)
         # frozen-plan (K6) state, created at hand-off
         self.k6 = None
         self.loss_dev = torch.zeros(1, dtype=f32, device=dev)
         torch.cuda.current_stream(self.dev).synchronize()
+
+    def _tabG_ld(self, F: int):
+        t = self._tabG_lds.get(F)
+        if t is None:
+            t = _dev(np.full(self.L.n_dev, F, np.int64), torch.int64, self.dev)
+            self._tabG_lds[F] = t
+        return t
 
     def stream(self) -> int:
         return torch.cuda.current_stream(self.dev).cuda_stream
@@ -388,11 +397,12 @@ class Engine:
             if kind == "gcn":
                 call("cg_gemm", n_in, Fo, F, ptr(self.Z[l]), F, self._p(2 * l), 0, None, 0, None,
                      0, self._p(2 * l + 1), 0 if last else 1,
-                     None if last else ptr(self.norm_src), ptr(out), Fo, self.gemm_mode, st)
+                     None if last else ptr(self.norm_src), None, 0, ptr(out), Fo,
+                     self.gemm_mode, st)
             else:
                 call("cg_gemm", n_in, Fo, F, ptr(self.X[l]), F, self._p(3 * l), F,
                      ptr(self.Z[l]), F, self._p(3 * l + 1), 0, self._p(3 * l + 2),
-                     0 if last else 1, None, ptr(out), Fo, self.gemm_mode, st)
+                     0 if last else 1, None, None, 0, ptr(out), Fo, self.gemm_mode, st)
         # ---------------- loss
         n_total = self.L.n
         loss_ptr = ptr(self.grads) + 4 * self.n_params
@@ -416,27 +426,51 @@ class Engine:
             if l == 0:
                 break
             nxt = self.dY[1 - cur] if l != nL - 1 else self.dY[cur]
-            if kind == "gcn":
-                call("cg_gemm", n_in, F, Fo, ptr(dY), Fo, self._p(2 * l), 0, None, 0, None, 1,
-                     None, 0, ptr(self.norm_dst), ptr(self.G), F, self.gemm_mode, st)
+            wide = Fo < F  # aggregate the narrower gradient, then transform
+            W = 2 * l if kind == "gcn" else 3 * l + 1
+            if wide:
+                # G = (b | 1/d_in) * dY  (F_out wide): the rows peers pull
+                call("cg_scale_rows_to", ptr(self.G), Fo, ptr(dY), Fo, n_in, Fo,
+                     ptr(self.norm_dst), st)
+                Fx = Fo
+            elif kind == "gcn":
+                call("cg_gemm", n_in, F, Fo, ptr(dY), Fo, self._p(W), 0, None, 0, None, 1,
+                     None, 0, ptr(self.norm_dst), None, 0, ptr(self.G), F, self.gemm_mode, st)
+                Fx = F
             else:
-                call("cg_gemm", n_in, F, Fo, ptr(dY), Fo, self._p(3 * l + 1), 0, None, 0, None,
-                     1, None, 0, ptr(self.norm_dst), ptr(self.G), F, self.gemm_mode, st)
+                call("cg_gemm", n_in, F, Fo, ptr(dY), Fo, self._p(W), 0, None, 0, None,
+                     1, None, 0, ptr(self.norm_dst), None, 0, ptr(self.G), F, self.gemm_mode, st)
                 call("cg_gemm", n_in, F, Fo, ptr(dY), Fo, self._p(3 * l), 0, None, 0, None, 1,
-                     None, 0, None, ptr(self.Hs), F, self.gemm_mode, st)
+                     None, 0, None, None, 0, ptr(self.Hs), F, self.gemm_mode, st)
+                Fx = F
             self.comm.barrier()
             if self.n_bwd:
-                self._copy(self.n_bwd, F, self.b_src, self.b_row, self.b_dst, self.tabG,
-                           self.tabG_ld[F], self.G, F)
+                self._copy(self.n_bwd, Fx, self.b_src, self.b_row, self.b_dst, self.tabG,
+                           self._tabG_ld(Fx), self.G, Fx)
             if timers:
                 a, b = mk(), mk()
                 a.record()
-            call("cg_spmm", n_in, F, ptr(self.bwd_rowptr), ptr(self.bwd_col), 1 << 62, None,
-                 ptr(self.G), F, ptr(self.norm_src) if kind == "gcn" else None,
-                 ptr(self.Hs) if kind == "sage" else None, F, ptr(self.X[l]), F, ptr(nxt), F, st)
+            if wide:
+                # T = (a | 1) * A^T G, then dY_{l-1} = mask * (T W^T [+ dY W_self^T])
+                call("cg_spmm", n_in, Fx, ptr(self.bwd_rowptr), ptr(self.bwd_col), 1 << 62, None,
+                     ptr(self.G), Fx, ptr(self.norm_src) if kind == "gcn" else None, None, 0,
+                     None, 0, ptr(self.T), Fx, st)
+            else:
+                call("cg_spmm", n_in, F, ptr(self.bwd_rowptr), ptr(self.bwd_col), 1 << 62, None,
+                     ptr(self.G), F, ptr(self.norm_src) if kind == "gcn" else None,
+                     ptr(self.Hs) if kind == "sage" else None, F, ptr(self.X[l]), F, ptr(nxt), F,
+                     st)
             if timers:
                 b.record()
                 bwd_ev.append((a, b))
+            if wide:
+                if kind == "gcn":
+                    call("cg_gemm", n_in, F, Fo, ptr(self.T), Fo, self._p(W), 0, None, 0, None, 1,
+                         None, 0, None, ptr(self.X[l]), F, ptr(nxt), F, self.gemm_mode, st)
+                else:
+                    call("cg_gemm", n_in, F, Fo, ptr(dY), Fo, self._p(3 * l), Fo, ptr(self.T), Fo,
+                         self._p(W), 1, None, 0, None, ptr(self.X[l]), F, ptr(nxt), F,
+                         self.gemm_mode, st)
             if l != nL - 1:
                 cur = 1 - cur
         # ---------------- K7 + optimizer

@@ -24,6 +24,21 @@ def workload(n, deg, P, hops=1, seed=0):
     return g, ps, og, ops
 
 
+def oracle_run_forced(og, ops, kind, f_dim, C, caps, policy, s, params_per_epoch, seed_w=2):
+    """Oracle epochs driven by the GPU's weights at the start of each epoch."""
+    verts, _, _, score = ohp.influence(og, ops)
+    ranked = ohp.ranked_halos(ops, verts, score)
+    imp = {int(v): float(x) for v, x in zip(verts, score)}
+    pr = ohp.plan_epochs(policy, (caps.c_cpu, tuple(caps.c_gpu), caps.bytes_per_entry),
+                         ranked, ops.halo, imp, len(params_per_epoch), s)
+    dims = list(f_dim) + [C]
+    tr = omp.Trainer(og, ops.inner, ops.halo, omp.ModelSpec(kind, dims),
+                     omp.features(og.n, dims[0], seed=0), omp.labels(og.n, C, seed=1),
+                     params=omp.init_params(kind, dims, seed_w))
+    outs = [tr.step(p.version, forced_params=w) for p, w in zip(pr.plans, params_per_epoch)]
+    return pr, outs
+
+
 def oracle_run(og, ops, kind, f_dim, C, caps, policy, s, epochs, seed_w=2):
     verts, _, _, score = ohp.influence(og, ops)
     ranked = ohp.ranked_halos(ops, verts, score)

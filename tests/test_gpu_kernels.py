@@ -99,7 +99,7 @@ def test_gemm_epilogue(shape):
     out = torch.zeros(M, N, device="cuda")
     k = [_t(A), _t(B), _t(A2), _t(B2), _t(bias), _t(rs)]
     call("cg_gemm", M, N, K, ptr(k[0]), K, ptr(k[1]), K, ptr(k[2]), K, ptr(k[3]), tb,
-         ptr(k[4]), 1, ptr(k[5]), ptr(out), N, 0, _st())
+         ptr(k[4]), 1, ptr(k[5]), None, 0, ptr(out), N, 0, _st())
     _sync()
     np.testing.assert_allclose(out.cpu().numpy(), ref, rtol=1e-4, atol=1e-3)
 
@@ -203,10 +203,14 @@ def test_gemm_tcgen05(shape, mode):
     if K2:
         ref += A2.astype(np.float64) @ (B2.T if tb else B2)
     ref = np.maximum(ref + bias, 0) * rs[:, None]
+    mask = rng.standard_normal((M, N + 4)).astype(np.float32) if K2 == 0 else None
+    if mask is not None:  # ReLU-backward style mask with its own leading dim
+        ref = np.where(mask[:, :N] > 0, ref, 0.0)
     out = torch.full((M, N), float("nan"), device="cuda")
-    k = [_t(A), _t(B), _t(A2) if K2 else None, _t(B2) if K2 else None, _t(bias), _t(rs)]
+    k = [_t(A), _t(B), _t(A2) if K2 else None, _t(B2) if K2 else None, _t(bias), _t(rs),
+         _t(mask) if mask is not None else None]
     call("cg_gemm", M, N, K1, ptr(k[0]), K1, ptr(k[1]), K2, ptr(k[2]), K2, ptr(k[3]), tb,
-         ptr(k[4]), 1, ptr(k[5]), ptr(out), N, mode, _st())
+         ptr(k[4]), 1, ptr(k[5]), ptr(k[6]), N + 4, ptr(out), N, mode, _st())
     _sync()
     got = out.cpu().numpy()
     scale = np.abs(ref).max()
