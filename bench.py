@@ -251,7 +251,10 @@ def run_ours(args):
                        "setup_s": round(t_setup, 2)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,
-                         "traffic": prof.get("dram_bytes_per_launch"),
+                         "traffic": prof.get("dram_bytes_per_epoch"),
+                         "traffic_basis": "per epoch (sum over the k_spmm launches of one "
+                                          "epoch, ncu --set full; profiles/spmm_traffic.json), "
+                                          "same basis as bytes_per_epoch",
                          "kernel": "k_spmm (fused cache-lookup + gather SpMM), all fwd+bwd "
                                    "launches of the timed epochs",
                          "bytes_per_epoch": sum(fb) + sum(bb),

@@ -62,6 +62,7 @@ class DistComm:
         self.backend = dist.get_backend()
         dev = torch.device("cuda", device) if self.backend == "nccl" else torch.device("cpu")
         self._flag = torch.zeros(1, dtype=torch.float32, device=dev)
+        self._cuda = torch.cuda.is_available()
         self._opened: list[int] = []
 
     def barrier(self) -> None:
@@ -69,7 +70,8 @@ class DistComm:
             self.dist.all_reduce(self._flag)   # stream-ordered device barrier
         else:
             import torch
-            torch.cuda.current_stream().synchronize()
+            if self._cuda:
+                torch.cuda.current_stream().synchronize()
             self.dist.barrier()
 
     def host_barrier(self) -> None:
@@ -77,6 +79,8 @@ class DistComm:
 
     def allreduce_(self, t) -> None:
         if self.backend == "nccl":
+            self.dist.all_reduce(t)
+        elif not t.is_cuda:
             self.dist.all_reduce(t)
         else:
             import torch
