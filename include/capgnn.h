@@ -95,11 +95,25 @@ int cg_spmm(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col,
  * trans_b = 1 means B is supplied as [N x K] row-major (use B^T).
  * epi: (+ bias[n]) -> (relu if relu) -> (* row_scale[m])
  *      -> (* (mask[m*ldm + n] > 0)) when mask != NULL (ReLU backward).
- * mode: 0 = fp32 SIMT, 1 = 3xTF32 tcgen05 (parity), 2 = 1xTF32 tcgen05.   */
+ * mode: 0 = fp32 SIMT, 1 = 3xTF32 tcgen05 (parity), 2 = 1xTF32 tcgen05.
+ * B1_lo / B2_lo (mode 1 only, optional): B is pre-split, B1 = tf32_hi(B),
+ * B1_lo = B - tf32_hi(B) (cg_split_tf32 / cg_adam outputs); the kernel then
+ * splits only the A operand.                                              */
 int cg_gemm(int64_t M, int N, int K1, const float *A1, int64_t lda1,
             const float *B1, int K2, const float *A2, int64_t lda2, const float *B2,
             int trans_b, const float *bias, int relu, const float *row_scale,
-            const float *mask, int64_t ldm, float *C, int64_t ldc, int mode, void *stream);
+            const float *mask, int64_t ldm, float *C, int64_t ldc, int mode,
+            const float *B1_lo, const float *B2_lo, void *stream);
+/* hi[i] = x[i] with the low 13 mantissa bits cleared (a TF32 value),
+ * lo[i] = x[i] - hi[i] (exact).                                           */
+int cg_split_tf32(int64_t n, const float *x, float *hi, float *lo, void *stream);
+/* The same split, transposed, for n_mats row-major matrices packed in one
+ * flat buffer: matrix m (rows[m] x cols[m]) at element offset off[m] of x
+ * is written as its transpose (cols x rows) at the same offset of hi / lo.
+ * off / rows / cols are DEVICE arrays.  Gives the forward transform a
+ * K-major (one TMA box per k-block) weight operand.                      */
+int cg_split_tf32_t(int n_mats, const int64_t *off, const int32_t *rows, const int32_t *cols,
+                    const float *x, float *hi, float *lo, int64_t max_elems, void *stream);
 /* dW[k, n] (+)= sum_m A[m, k] * D[m, n]; deterministic split over m.
  * ws must hold cg_wgrad_workspace(M, K, N) floats.                        */
 int64_t cg_wgrad_workspace(int64_t M, int K, int N);
@@ -117,8 +131,11 @@ int cg_softmax_ce(int64_t n_rows, int C, const float *logits, int64_t ld,
                   float *loss_out, float *ws, void *stream);
 
 /* ---- optimizer (replicated on every rank after the K7 all-reduce) ------ */
+/* p_hi / p_lo (optional): also emit the TF32 split of the updated params
+ * (as cg_split_tf32) for the pre-split 3xTF32 GEMM operands.              */
 int cg_adam(int64_t n, float *param, const float *grad, float *m, float *v,
-            float lr, float beta1, float beta2, float eps, int step, void *stream);
+            float lr, float beta1, float beta2, float eps, int step, float *p_hi,
+            float *p_lo, void *stream);
 
 /* ---- K6: frozen-membership JACA/FIFO plan for one epoch ---------------- *
  * One thread per halo-union vertex u; requesters of u (partition slots whose

@@ -50,12 +50,15 @@ SIGNATURES = {
     "cg_scale_rows_to": [P, I64, P, I64, I64, INT, P, P],
     "cg_copy_rows": [I64, INT, P, P, P, P, P, P, I64, P],
     "cg_spmm": [I64, INT, P, P, I64, P, P, I64, P, P, I64, P, I64, P, I64, P],
-    "cg_gemm": [I64, INT, INT, P, I64, P, INT, P, I64, P, INT, P, INT, P, P, I64, P, I64, INT, P],
+    "cg_gemm": [I64, INT, INT, P, I64, P, INT, P, I64, P, INT, P, INT, P, P, I64, P, I64, INT,
+                P, P, P],
+    "cg_split_tf32": [I64, P, P, P, P],
+    "cg_split_tf32_t": [INT, P, P, P, P, P, P, I64, P],
     "cg_wgrad_workspace": [I64, INT, INT],
     "cg_wgrad": [I64, INT, INT, P, I64, P, I64, P, P, INT, P],
     "cg_colsum": [I64, INT, P, I64, P, P, P],
     "cg_softmax_ce": [I64, INT, P, I64, P, F32, P, I64, P, P, P],
-    "cg_adam": [I64, P, P, P, P, F32, F32, F32, F32, INT, P],
+    "cg_adam": [I64, P, P, P, P, F32, F32, F32, F32, INT, P, P, P],
     "cg_plan_frozen": [P, INT, INT, INT, P, P, P, P, P, P, P, P, P, I32, I32, P, P],
     "cg_planner_create": [INT, INT, I64, P, I64, P, P],
     "cg_planner_destroy": [P],
@@ -113,6 +116,7 @@ def lib():
 KERNEL_ENTRY = {"cg_hash_features", "cg_hash_labels", "cg_scale_rows", "cg_scale_rows_to",
                 "cg_copy_rows",
                 "cg_spmm", "cg_gemm", "cg_wgrad", "cg_colsum", "cg_softmax_ce", "cg_adam",
+                "cg_split_tf32", "cg_split_tf32_t",
                 "cg_plan_frozen"}
 launches = {"total": 0}
 

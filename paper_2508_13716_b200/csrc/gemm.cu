@@ -20,7 +20,7 @@ extern int cg_cuda_fail(cudaError_t e, const char *what);
 int cg_gemm_tc(int64_t M, int N, int K1, const float *A1, int64_t lda1, const float *B1, int K2,
                const float *A2, int64_t lda2, const float *B2, int trans_b, const float *bias,
                int relu, const float *row_scale, const float *mask, int64_t ldm, float *C,
-               int64_t ldc, int mode, cudaStream_t st);
+               int64_t ldc, int mode, const float *B1_lo, const float *B2_lo, cudaStream_t st);
 int cg_wgrad_tc(int64_t M, int K, int N, const float *A, int64_t lda, const float *D, int64_t ldd,
                 float *ws, int64_t chunk, int64_t n_chunks, int mode, cudaStream_t st);
 
@@ -176,7 +176,17 @@ __global__ void k_wgrad_reduce(int64_t n_out, int64_t n_chunks, const float *__r
     out[i] = (s0 + s1) + (s2 + s3);
 }
 
-constexpr int64_t kWgradChunk = 1024;  // short TC accumulation chains (accuracy), many CTAs
+constexpr int64_t kWgradChunk = 1024;  // minimum split-K chunk (SIMT path: always this)
+
+// Tensor-core split-K chunk: enough (k, n, chunk) tiles for ~2 per SM, fewer
+// partials for the reduction; a multiple of the 32-row k-block.
+int64_t wgrad_chunk_tc(int64_t M, int K, int N) {
+    const int64_t tiles_mn = ((K + 127) / 128) * ((N + 127) / 128);
+    int64_t n_z = (2 * 148 + tiles_mn - 1) / tiles_mn;
+    int64_t chunk = (M + n_z - 1) / n_z;
+    chunk = (chunk + 31) / 32 * 32;
+    return chunk < kWgradChunk ? kWgradChunk : chunk;
+}
 
 }  // namespace
 
@@ -185,11 +195,12 @@ extern "C" {
 int cg_gemm(int64_t M, int N, int K1, const float *A1, int64_t lda1, const float *B1, int K2,
             const float *A2, int64_t lda2, const float *B2, int trans_b, const float *bias,
             int relu, const float *row_scale, const float *mask, int64_t ldm, float *C,
-            int64_t ldc, int mode, void *stream) {
+            int64_t ldc, int mode, const float *B1_lo, const float *B2_lo, void *stream) {
     if (M == 0 || N == 0) return 0;
     if (mode != 0)
         return cg_gemm_tc(M, N, K1, A1, lda1, B1, K2, A2, lda2, B2, trans_b, bias, relu,
-                          row_scale, mask, ldm, C, ldc, mode, (cudaStream_t)stream);
+                          row_scale, mask, ldm, C, ldc, mode, B1_lo, B2_lo,
+                          (cudaStream_t)stream);
     dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN));
     k_gemm<<<grid, NT, 0, (cudaStream_t)stream>>>(M, N, K1, A1, lda1, B1, K2, A2, lda2, B2,
                                                  trans_b, bias, relu, row_scale, mask, ldm,
@@ -208,11 +219,12 @@ int cg_wgrad(int64_t M, int K, int N, const float *A, int64_t lda, const float *
              float *dW, float *ws, int mode, void *stream) {
     if (K == 0 || N == 0) return 0;
     cudaStream_t st = (cudaStream_t)stream;
-    int64_t nch = (M + kWgradChunk - 1) / kWgradChunk;
+    const int64_t chunk = (mode == 1 || mode == 2) ? wgrad_chunk_tc(M, K, N) : kWgradChunk;
+    int64_t nch = (M + chunk - 1) / chunk;
     if (nch < 1) nch = 1;
     int launched = 0;
     if (mode == 1 || mode == 2) {
-        int rc = cg_wgrad_tc(M, K, N, A, lda, D, ldd, ws, kWgradChunk, nch, mode, st);
+        int rc = cg_wgrad_tc(M, K, N, A, lda, D, ldd, ws, chunk, nch, mode, st);
         if (rc < 0) return rc;
         launched += rc;
     } else {

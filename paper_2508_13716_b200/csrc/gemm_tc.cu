@@ -37,13 +37,13 @@ namespace tc {
 constexpr int BM = 128;          // UMMA M (cta_group::1)
 constexpr int BK = 32;           // fp32 elements per 128-byte swizzle row
 constexpr int UK = 8;            // K per tcgen05.mma kind::tf32
-constexpr int BN_MAX = 256;
+constexpr int BN_MAX = 256;     // TMEM columns per accumulator buffer (1xTF32 tiles)
+constexpr int BN_MAX_3X = 128;  // 3xTF32 tiles: smaller B slices buy a deeper stage ring
 constexpr int A_BYTES = BM * BK * 4;             // 16 KB A operand stage
-constexpr int B_BYTES = BN_MAX * BK * 4;         // 32 KB B operand stage
-constexpr int HI_BYTES = A_BYTES + B_BYTES;      // [A | B]
-constexpr int STAGE_BYTES_1X = HI_BYTES;         // A, B
-constexpr int STAGE_BYTES_3X = 2 * HI_BYTES;     // A, B, A_lo, B_lo (lo = hi + HI_BYTES)
-constexpr int EPI_BYTES = 4 * 32 * 33 * 4;  // epilogue transpose staging
+constexpr int EPI_BYTES = 4 * 2 * 4096;     // per epilogue warp: 2 x (32 rows x 128 B) TMA-store staging
+constexpr int SMEM_LIMIT = 227 * 1024;
+constexpr int SMEM_FIXED = 1024 + EPI_BYTES;  // barriers, epilogue staging
+// Stage layout: [A | B] (hi) and, for 3xTF32, [A_lo | B_lo] at +hi_bytes.
 constexpr int THREADS = 384;  // 12 warps: TMA, MMA, -, -, 4 epilogue, 4 splitter
 
 struct Op {
@@ -65,8 +65,17 @@ struct Params {
     float *C;
     int64_t ldc;
     int split3;      // 3xTF32
+    int b_presplit;  // 3xTF32 with B supplied as (hi, lo) tensors: split A only
     int stages;
-    int BN;          // UMMA N (multiple of 16, <= 128)
+    int hi_bytes;    // bytes of [A | B] in one stage (1024-aligned)
+    int BN;          // UMMA N (multiple of 16)
+    int vec_ok;      // C / mask / bias rows 16-byte aligned: float4 epilogue
+    int a_tmem;      // 3xTF32, K-major A: the splitter moves A and A_lo into TMEM
+                     // (tcgen05.mma A-from-TMEM), so smem carries only B traffic
+    int stage_bytes;
+    int b_lo_off;    // offset of B_lo from the B slice in a stage
+    int acc_stride;  // TMEM columns between the two accumulator buffers
+    int tma_store;   // C written by TMA bulk tensor stores (mC is valid)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -101,6 +110,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     } while (!done);
 }
 
+__device__ __forceinline__ bool elect_one() {
+    uint32_t e;
+    asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(e));
+    return e != 0;
+}
+
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap *map, uint64_t *bar, void *dst,
                                             int x, int y) {
     asm volatile(
@@ -132,6 +148,75 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t a_tmem, uint64_t b,
+                                            uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),
+        "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]),
+        "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]),
+        "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+        "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+
+// C tile store: smem (128B-swizzled, 32 rows x 32 fp32) -> global via TMA;
+// the tensor map clips rows >= M and columns >= N.
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, const void *src, int x, int y,
+                                             int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z)
+        : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+// One k-block (BK = 4 UMMA k-steps) issued by the elected lane of a
+// converged warp, with the descriptor / TMEM-column increments done in PTX:
+// keeps the issuing warp's per-UMMA overhead to a few instructions (a lone
+// thread re-materialises every operand into uniform registers per UMMA).
+// ts3: 3xTF32 with A, A_lo in TMEM columns [ta, ta+32): A_lo.B_hi, A.B_lo, A.B_hi
+__device__ __forceinline__ void mma_kblock_ts3(uint32_t d, uint32_t ta, uint64_t db, uint64_t dbl,
+                                               uint64_t bstep, uint32_t idesc, uint32_t acc,
+                                               uint64_t *bar) {
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t.reg .b64 b1, b2, b3, l1, l2, l3;\n\t"
+        ".reg .b32 a0, a1, a2, a3, o0, o1, o2, o3;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "add.s64 b1, %2, %4; add.s64 b2, b1, %4; add.s64 b3, b2, %4;\n\t"
+        "add.s64 l1, %3, %4; add.s64 l2, l1, %4; add.s64 l3, l2, %4;\n\t"
+        "add.u32 a1, %1, 8; add.u32 a2, %1, 16; add.u32 a3, %1, 24;\n\t"
+        "add.u32 o0, %1, 32; add.u32 o1, %1, 40; add.u32 o2, %1, 48; add.u32 o3, %1, 56;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [o0], %2, %5, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [o1], b1, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a1], l1, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a1], b1, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [o2], b2, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a2], l2, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a2], b2, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [o3], b3, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a3], l3, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a3], b3, %5, 1;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n\t}"
+        ::"r"(d), "r"(ta), "l"(db), "l"(dbl), "l"(bstep), "r"(idesc), "r"(acc),
+        "r"(smem_u32(bar))
+        : "memory");
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
@@ -195,22 +280,25 @@ __device__ __forceinline__ void kblocks(const Params &p, int o, int z, int &begi
 __global__ void __launch_bounds__(THREADS, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mB0,
           const __grid_constant__ CUtensorMap mA1, const __grid_constant__ CUtensorMap mB1,
-          const Params p) {
+          const __grid_constant__ CUtensorMap mBl0, const __grid_constant__ CUtensorMap mBl1,
+          const __grid_constant__ CUtensorMap mC, const Params p) {
     // no static shared memory in this kernel, so the dynamic window starts
     // 1024-byte aligned (required by the 128B-swizzle atoms); pointers stay
     // derived from the __shared__ array so accesses compile to LDS/STS
     extern __shared__ __align__(1024) uint8_t smem[];
     const int S = p.stages;
-    const int stage_bytes = p.split3 ? STAGE_BYTES_3X : STAGE_BYTES_1X;
+    const int HI_BYTES = p.hi_bytes;
+    const int stage_bytes = p.stage_bytes;
+    const uint32_t A_TMEM_COL = 2 * p.acc_stride;  // A / A_lo stage slots follow the accumulators
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + S * stage_bytes);
     uint64_t *conv = full + S;
     uint64_t *empty = conv + S;
     uint64_t *tfull = empty + S;   // [2] accumulator ready
     uint64_t *tempty = tfull + 2;  // [2] accumulator drained
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
-    float *epi_stage = reinterpret_cast<float *>(smem + S * stage_bytes + 1024);  // 4 x 32x33
 
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    // warp index made provably warp-uniform (shfl) so role branches do not diverge
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
     const int n_tiles = (p.N + p.BN - 1) / p.BN;
     const int64_t m_tiles = (p.M + BM - 1) / BM;
     const int64_t n_z = p.k_chunk > 0 ? (p.op[0].K + p.k_chunk - 1) / p.k_chunk : 1;
@@ -240,8 +328,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
     const uint32_t tmem_base = *tmem_slot;
     const int nb_b = (p.BN + 31) / 32;  // 32-column boxes for an MN-major B
 
-    if (warp == 0 && lane == 0) {
-        // ------------------------------------------------ TMA producer
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer (converged
+        // warp; the elected lane issues)
         uint32_t it = 0;
         for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
             const TileCoord tc = tile_of(p, t, n_tiles, m_tiles);
@@ -250,6 +339,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                 kblocks(p, o, tc.z, kb0, nkb);
                 const CUtensorMap *ma = o ? &mA1 : &mA0;
                 const CUtensorMap *mb = o ? &mB1 : &mB0;
+                const CUtensorMap *mbl = o ? &mBl1 : &mBl0;
                 const uint32_t bbytes = p.op[o].b_mn ? nb_b * 32 * BK * 4 : p.BN * BK * 4;
                 for (int kb = kb0; kb < kb0 + nkb; ++kb, ++it) {
                     const int s = it % S;
@@ -257,7 +347,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                     const int k0 = kb * BK;
                     uint8_t *sa = smem + s * stage_bytes;
                     uint8_t *sb = sa + A_BYTES;
-                    mbar_expect_tx(&full[s], A_BYTES + bbytes);
+                    if (elect_one()) {
+                    mbar_expect_tx(&full[s], A_BYTES + bbytes * (p.b_presplit ? 2 : 1));
                     if (p.op[o].a_mn) {
                         for (int b = 0; b < 4; ++b)
                             tma_load_2d(ma, &full[s], sa + b * 4096, (int)(tc.m0 + 32 * b), k0);
@@ -265,29 +356,38 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                         tma_load_2d(ma, &full[s], sa, k0, (int)tc.m0);
                     }
                     if (p.op[o].b_mn) {
-                        for (int b = 0; b < nb_b; ++b)
+                        for (int b = 0; b < nb_b; ++b) {
                             tma_load_2d(mb, &full[s], sb + b * 4096, tc.n0 + 32 * b, k0);
+                            if (p.b_presplit)
+                                tma_load_2d(mbl, &full[s], sb + p.b_lo_off + b * 4096,
+                                            tc.n0 + 32 * b, k0);
+                        }
                     } else {
                         tma_load_2d(mb, &full[s], sb, k0, tc.n0);
+                        if (p.b_presplit) tma_load_2d(mbl, &full[s], sb + p.b_lo_off, k0, tc.n0);
                     }
+                    }
+                    __syncwarp();
                 }
             }
         }
-    } else if (warp == 1 && lane == 0) {
-        // ------------------------------------------------ MMA issuer
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer (converged
+        // warp; one elected lane issues inside mma_kblock_*; the others idle)
         uint32_t it = 0, ti = 0;
         for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++ti) {
             const TileCoord tc = tile_of(p, t, n_tiles, m_tiles);
             const uint32_t acc_buf = ti & 1;
             mbar_wait(&tempty[acc_buf], ((ti >> 1) & 1) ^ 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t tmem_d = tmem_base + acc_buf * BN_MAX;
+            const uint32_t tmem_d = tmem_base + acc_buf * p.acc_stride;
             bool first = true;
             for (int o = 0; o < p.n_ops; ++o) {
                 int kb0, nkb;
                 kblocks(p, o, tc.z, kb0, nkb);
                 const int a_mn = p.op[o].a_mn, b_mn = p.op[o].b_mn;
-                const uint32_t idesc = instr_desc(a_mn, b_mn, p.BN);
+                // an A operand in TMEM is always K-major (lane = row, column = k)
+                const uint32_t idesc = instr_desc(p.a_tmem ? 0 : a_mn, b_mn, p.BN);
                 // K-major (SW128): 8-row x 128 B atoms, SBO = 1024, k-step = +32 B.
                 // MN-major (SW128, 32 B atoms): 4-row x 128 B atoms, SBO = 512
                 // between K groups, LBO = 4096 between the 32-wide MN boxes,
@@ -304,7 +404,18 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     const uint32_t sa = smem_u32(smem + s * stage_bytes);
                     const uint32_t sb = sa + A_BYTES;
-                    const uint32_t sa_lo = sa + HI_BYTES, sb_lo = sb + HI_BYTES;
+                    const uint32_t sa_lo = sa + HI_BYTES, sb_lo = sb + p.b_lo_off;
+                    if (p.a_tmem) {
+                        // A (= its TF32 truncation) and A_lo sit in TMEM slot s
+                        mma_kblock_ts3(tmem_d, tmem_base + A_TMEM_COL + 64 * s,
+                                       smem_desc(sb, b_lbo, b_sbo, b_lay),
+                                       smem_desc(sb_lo, b_lbo, b_sbo, b_lay), b_step >> 4, idesc,
+                                       first ? 0u : 1u, &empty[s]);
+                        first = false;
+                        __syncwarp();
+                        continue;
+                    }
+                    if (lane == 0) {
 #pragma unroll
                     for (int j = 0; j < BK / UK; ++j) {
                         const uint64_t da = smem_desc(sa + j * a_step, a_lbo, a_sbo, a_lay);
@@ -322,58 +433,142 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                         }
                     }
                     mma_commit(&empty[s]);  // frees the smem slot once these MMAs retire
+                    }
+                    first = false;
+                    __syncwarp();
                 }
             }
-            mma_commit(&tfull[acc_buf]);
+            if (lane == 0) mma_commit(&tfull[acc_buf]);
+            __syncwarp();
         }
     } else if (warp >= 4 && warp < 8) {
         // ------------------------------------------------ epilogue
-        // Warp q owns TMEM lanes (= tile rows) 32q..32q+31.  Each 32x32
-        // sub-tile goes TMEM -> registers (thread = row) -> padded smem ->
-        // registers (lane = column), so bias / mask loads and the output
-        // stores are 128-byte coalesced row segments.
+        // Warp q owns TMEM lanes 32q..32q+31 = tile rows; thread = one output
+        // row.  Each 32-column chunk goes TMEM -> 32 registers -> bias / ReLU
+        // / row scale / ReLU-backward mask -> eight 16-byte stores of the
+        // row's 128-byte segment (no transposes, ~4 instructions per float4).
         const int q = warp & 3;
-        float (*stg)[33] = reinterpret_cast<float (*)[33]>(epi_stage + q * 32 * 33);
-        uint32_t ti = 0;
+        uint8_t *stg0 = smem + S * stage_bytes + 1024 + q * 8192;  // this warp's 2 staging buffers
+        uint32_t ti = 0, nst = 0;
         for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++ti) {
             const TileCoord tc = tile_of(p, t, n_tiles, m_tiles);
             const uint32_t acc_buf = ti & 1;
             mbar_wait(&tfull[acc_buf], (ti >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const int64_t row0 = tc.m0 + 32 * q;
+            const int64_t row = tc.m0 + 32 * q + lane;
+            const bool row_ok = row < p.M;
             float *cbase = p.k_chunk > 0 ? p.C + (int64_t)tc.z * p.M * p.ldc : p.C;
-            const float rs_lane =
-                (p.row_scale && row0 + lane < p.M) ? p.row_scale[row0 + lane] : 1.f;
+            float *crow = cbase + (row_ok ? row : 0) * p.ldc + tc.n0;
+            const float *mrow = p.mask ? p.mask + (row_ok ? row : 0) * p.ldm + tc.n0 : nullptr;
+            const float rs = (p.row_scale && row_ok) ? p.row_scale[row] : 1.f;
+            const float *brow = p.bias ? p.bias + tc.n0 : nullptr;
             for (int c0 = 0; c0 < p.BN; c0 += 32) {
-                const int n = tc.n0 + c0 + lane;
-                const bool col_ok = n < p.N && c0 + lane < p.BN;
-                // issue the global loads first so they overlap the TMEM read
-                float mk[32];
-                if (p.mask) {
-#pragma unroll
-                    for (int r = 0; r < 32; ++r)
-                        mk[r] = (col_ok && row0 + r < p.M) ? p.mask[(row0 + r) * p.ldm + n] : 1.f;
-                }
-                const float bias = (p.bias && col_ok) ? p.bias[n] : 0.f;
                 float v[32];
-                tmem_ld32(tmem_base + acc_buf * BN_MAX + ((uint32_t)(32 * q) << 16) + c0, v);
+                tmem_ld32(tmem_base + acc_buf * p.acc_stride + ((uint32_t)(32 * q) << 16) + c0, v);
+                int ncol = p.N - (tc.n0 + c0);
+                if (ncol > p.BN - c0) ncol = p.BN - c0;
+                if (ncol > 32) ncol = 32;
+                if (ncol <= 0) continue;
+                if (p.tma_store) {
+                    // apply the epilogue in registers, stage the 32 x 32 block
+                    // (swizzled: chunk j of row r at j ^ (r & 7)), one TMA store
+                    const uint32_t stg = smem_u32(stg0 + (nst & 1) * 4096);
+                    // issue the row's mask loads before anything waits
+                    float4 mk[8];
+                    if (mrow && row_ok) {
 #pragma unroll
-                for (int i = 0; i < 32; ++i) stg[lane][i] = v[i];
-                __syncwarp();
+                        for (int j = 0; j < 8; ++j) {
+                            if (4 * j >= ncol) {
+                                mk[j] = make_float4(1.f, 1.f, 1.f, 1.f);
+                            } else if (p.vec_ok) {
+                                mk[j] = __ldg(reinterpret_cast<const float4 *>(mrow + c0) + j);
+                            } else {
+                                const int cb = c0 + 4 * j;
+                                mk[j].x = mrow[cb];
+                                mk[j].y = 4 * j + 1 < ncol ? mrow[cb + 1] : 0.f;
+                                mk[j].z = 4 * j + 2 < ncol ? mrow[cb + 2] : 0.f;
+                                mk[j].w = 4 * j + 3 < ncol ? mrow[cb + 3] : 0.f;
+                            }
+                        }
+                    }
+                    if (lane == 0)  // the store that used this buffer 2 chunks ago has read it
+                        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                    __syncwarp();
 #pragma unroll
-                for (int r = 0; r < 32; ++r) {
-                    const int64_t row = row0 + r;
-                    float y = stg[r][lane] + bias;
-                    if (p.relu) y = fmaxf(y, 0.f);
-                    y *= __shfl_sync(0xffffffffu, rs_lane, r);
-                    if (p.mask && !(mk[r] > 0.f)) y = 0.f;
-                    if (col_ok && row < p.M) cbase[row * p.ldc + n] = y;
+                    for (int j = 0; j < 8; ++j) {
+                        float4 bb = make_float4(0.f, 0.f, 0.f, 0.f);
+                        if (brow) {
+                            if (p.vec_ok) {
+                                bb = __ldg(reinterpret_cast<const float4 *>(brow + c0) + j);
+                            } else {
+                                const int cb = c0 + 4 * j;
+                                bb.x = 4 * j < ncol ? brow[cb] : 0.f;
+                                bb.y = 4 * j + 1 < ncol ? brow[cb + 1] : 0.f;
+                                bb.z = 4 * j + 2 < ncol ? brow[cb + 2] : 0.f;
+                                bb.w = 4 * j + 3 < ncol ? brow[cb + 3] : 0.f;
+                            }
+                        }
+                        float4 y = make_float4(v[4 * j] + bb.x, v[4 * j + 1] + bb.y,
+                                               v[4 * j + 2] + bb.z, v[4 * j + 3] + bb.w);
+                        if (p.relu) {
+                            y.x = fmaxf(y.x, 0.f); y.y = fmaxf(y.y, 0.f);
+                            y.z = fmaxf(y.z, 0.f); y.w = fmaxf(y.w, 0.f);
+                        }
+                        y.x *= rs; y.y *= rs; y.z *= rs; y.w *= rs;
+                        if (mrow && row_ok) {
+                            const float4 m = mk[j];
+                            y.x = m.x > 0.f ? y.x : 0.f; y.y = m.y > 0.f ? y.y : 0.f;
+                            y.z = m.z > 0.f ? y.z : 0.f; y.w = m.w > 0.f ? y.w : 0.f;
+                        }
+                        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                         stg + lane * 128 + 16 * (j ^ (lane & 7))),
+                                     "f"(y.x), "f"(y.y), "f"(y.z), "f"(y.w)
+                                     : "memory");
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0)
+                        tma_store_3d(&mC, stg0 + (nst & 1) * 4096, tc.n0 + c0,
+                                     (int)(tc.m0 + 32 * q), tc.z);
+                    ++nst;
+                    continue;
                 }
-                __syncwarp();
+                if (!row_ok) continue;
+                if (ncol == 32 && p.vec_ok) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        float4 bb = brow ? __ldg(reinterpret_cast<const float4 *>(brow + c0) + j)
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+                        float4 y = make_float4(v[4 * j] + bb.x, v[4 * j + 1] + bb.y,
+                                               v[4 * j + 2] + bb.z, v[4 * j + 3] + bb.w);
+                        if (p.relu) {
+                            y.x = fmaxf(y.x, 0.f); y.y = fmaxf(y.y, 0.f);
+                            y.z = fmaxf(y.z, 0.f); y.w = fmaxf(y.w, 0.f);
+                        }
+                        y.x *= rs; y.y *= rs; y.z *= rs; y.w *= rs;
+                        if (mrow) {
+                            const float4 m = __ldg(reinterpret_cast<const float4 *>(mrow + c0) + j);
+                            y.x = m.x > 0.f ? y.x : 0.f; y.y = m.y > 0.f ? y.y : 0.f;
+                            y.z = m.z > 0.f ? y.z : 0.f; y.w = m.w > 0.f ? y.w : 0.f;
+                        }
+                        reinterpret_cast<float4 *>(crow + c0)[j] = y;
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        if (i >= ncol) break;
+                        float y = v[i] + (brow ? brow[c0 + i] : 0.f);
+                        if (p.relu) y = fmaxf(y, 0.f);
+                        y *= rs;
+                        if (mrow && !(mrow[c0 + i] > 0.f)) y = 0.f;
+                        crow[c0 + i] = y;
+                    }
+                }
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             mbar_arrive(&tempty[acc_buf]);
         }
+        if (p.tma_store && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     } else if (warp >= 8 && p.split3) {
         // ------------------------------------------------ hi/lo split (3xTF32)
         const int t128 = threadIdx.x - 256;
@@ -386,10 +581,69 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
                     const int s = it % S;
                     mbar_wait(&full[s], (it / S) & 1);
-                    uint4 *hi = reinterpret_cast<uint4 *>(smem + s * stage_bytes);
+                    if (p.a_tmem) {
+                        const int q = warp & 3, r = 32 * q + lane;
+                        uint32_t hv[32], lv[32];
+                        if (!p.op[o].a_mn) {
+                            // thread = tile row r (TMEM lane): its 32 K values from
+                            // the 128B-swizzled K-major A tile (16-byte chunk c of
+                            // row r sits at chunk c ^ (r & 7))
+                            const uint8_t *rowp = smem + s * stage_bytes + r * 128;
+#pragma unroll
+                            for (int c = 0; c < 8; ++c) {
+                                const uint4 w = *reinterpret_cast<const uint4 *>(rowp + 16 * (c ^ (r & 7)));
+                                hv[4 * c] = w.x; hv[4 * c + 1] = w.y; hv[4 * c + 2] = w.z; hv[4 * c + 3] = w.w;
+                            }
+                        } else {
+                            // MN-major A (weight gradient: rows = features, K =
+                            // vertices): box q holds features 32q..32q+31, one
+                            // 128 B row per vertex, 32-byte atoms swizzled as
+                            // atom c of row v at c ^ (v & 3) (CuTe Swizzle<2,5,2>)
+                            const uint8_t *boxp = smem + s * stage_bytes + q * 4096;
+                            const int c = lane >> 3, w4 = (lane & 7) * 4;
+#pragma unroll
+                            for (int v = 0; v < 32; ++v)
+                                hv[v] = *reinterpret_cast<const uint32_t *>(
+                                    boxp + v * 128 + 32 * (c ^ (v & 3)) + w4);
+                        }
+                        if (!p.b_presplit) {
+                            // activations as B (weight gradient): B_lo in smem
+                            const int nb16 = (p.op[o].b_mn ? nb_b * 32 * BK * 4 : p.BN * BK * 4) / 16;
+                            const uint4 *bh = reinterpret_cast<const uint4 *>(smem + s * stage_bytes + A_BYTES);
+                            uint4 *bl = reinterpret_cast<uint4 *>(smem + s * stage_bytes + A_BYTES + p.b_lo_off);
+                            const int t128 = threadIdx.x - 256;
+#pragma unroll 4
+                            for (int i = t128; i < nb16; i += 128) {
+                                const uint4 w = bh[i];
+                                bl[i] = make_uint4(
+                                    __float_as_uint(__uint_as_float(w.x) - __uint_as_float(w.x & 0xFFFFE000u)),
+                                    __float_as_uint(__uint_as_float(w.y) - __uint_as_float(w.y & 0xFFFFE000u)),
+                                    __float_as_uint(__uint_as_float(w.z) - __uint_as_float(w.z & 0xFFFFE000u)),
+                                    __float_as_uint(__uint_as_float(w.w) - __uint_as_float(w.w & 0xFFFFE000u)));
+                            }
+                            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        }
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            lv[i] = __float_as_uint(__uint_as_float(hv[i]) -
+                                                    __uint_as_float(hv[i] & 0xFFFFE000u));
+                        const uint32_t ta = tmem_base + ((uint32_t)(32 * q) << 16) + A_TMEM_COL + 64 * s;
+                        tmem_st32(ta, hv);
+                        tmem_st32(ta + 32, lv);
+                        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                        mbar_arrive(&conv[s]);
+                        continue;
+                    }
+                    // the tensor core truncates fp32 operands to TF32 (measured:
+                    // tests/diag_tf32_rounding.py), so the raw tile already acts
+                    // as x_hi; only x_lo = x - trunc_tf32(x) is materialised
+                    const uint4 *hi = reinterpret_cast<const uint4 *>(smem + s * stage_bytes);
                     uint4 *lo = reinterpret_cast<uint4 *>(smem + s * stage_bytes + HI_BYTES);
-                    const int n16 =
-                        (A_BYTES + (p.op[o].b_mn ? nb_b * 32 * BK * 4 : p.BN * BK * 4)) / 16;
+                    // B arrives pre-split (weights) or is split here (activations)
+                    const int n16 = p.b_presplit
+                        ? A_BYTES / 16
+                        : (A_BYTES + (p.op[o].b_mn ? nb_b * 32 * BK * 4 : p.BN * BK * 4)) / 16;
 #pragma unroll 4
                     for (int i = t128; i < n16; i += 128) {
                         uint4 w = hi[i];
@@ -400,7 +654,6 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                             __float_as_uint(__uint_as_float(w.y) - __uint_as_float(h.y)),
                             __float_as_uint(__uint_as_float(w.z) - __uint_as_float(h.z)),
                             __float_as_uint(__uint_as_float(w.w) - __uint_as_float(h.w)));
-                        hi[i] = h;
                         lo[i] = l;
                     }
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -454,16 +707,63 @@ bool make_map(CUtensorMap *m, const float *ptr, int64_t inner, int64_t outer, in
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// C viewed as [n_z][M][N] (row stride ldc, z stride M*ldc), box 32 x 32 x 1.
+bool make_map_c(CUtensorMap *m, float *C, int64_t M, int N, int64_t ldc, int64_t n_z) {
+    encode_fn_t enc = encoder();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)M, (cuuint64_t)n_z};
+    cuuint64_t strides[2] = {(cuuint64_t)ldc * 4, (cuuint64_t)(M * ldc * 4)};
+    cuuint32_t box[3] = {32u, 32u, 1u};
+    cuuint32_t estr[3] = {1u, 1u, 1u};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, C, dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int launch(const Params &p0, const CUtensorMap &a0, const CUtensorMap &b0, const CUtensorMap &a1,
-           const CUtensorMap &b1, int grid_z, cudaStream_t st) {
+           const CUtensorMap &b1, const CUtensorMap &bl0, const CUtensorMap &bl1, int grid_z,
+           cudaStream_t st) {
     Params p = p0;
-    const int stage_bytes = p.split3 ? STAGE_BYTES_3X : STAGE_BYTES_1X;
-    p.stages = p.split3 ? 2 : 4;
-    const size_t smem = (size_t)p.stages * stage_bytes + 1024 + 1024 + EPI_BYTES;
+    CUtensorMap mc;
+    memset(&mc, 0, sizeof(mc));
+    static const bool no_tma_store = getenv("CG_GEMM_NO_TMA_STORE") != nullptr;  // experiment knob
+    p.tma_store = !no_tma_store && !(p.ldc % 4) && !((uintptr_t)p.C % 16) &&
+                  make_map_c(&mc, p.C, p.M, p.N, p.ldc, grid_z);
+    // B slice: MN-major B is loaded in 32-column boxes of 4 KB each
+    int b_bytes = 0;
+    for (int o = 0; o < p.n_ops; ++o) {
+        const int bb = p.op[o].b_mn ? ((p.BN + 31) / 32) * 32 * BK * 4 : p.BN * BK * 4;
+        b_bytes = bb > b_bytes ? bb : b_bytes;
+    }
+    b_bytes = (b_bytes + 1023) / 1024 * 1024;
+    p.hi_bytes = A_BYTES + b_bytes;
+    // 3xTF32: A and A_lo go to TMEM (split by the splitter warps), B_lo is
+    // either TMA-loaded (pre-split weights) or split into smem
+    p.a_tmem = p.split3 && p.BN <= 128;
+    if (p.a_tmem) {
+        p.stage_bytes = A_BYTES + 2 * b_bytes;  // [A | B_hi | B_lo]
+        p.b_lo_off = b_bytes;
+        p.acc_stride = 128;
+    } else {
+        p.stage_bytes = p.split3 ? 2 * p.hi_bytes : p.hi_bytes;  // [A | B] [A_lo | B_lo]
+        p.b_lo_off = p.hi_bytes;
+        p.acc_stride = BN_MAX;
+    }
+    const int stage_bytes = p.stage_bytes;
+    int stages = (SMEM_LIMIT - SMEM_FIXED) / stage_bytes;
+    static const int env_stages = getenv("CG_GEMM_STAGES") ? atoi(getenv("CG_GEMM_STAGES")) : 0;
+    int cap = env_stages > 0 ? env_stages : 6;   // experiment knob
+    if (p.a_tmem && cap > 4) cap = 4;            // TMEM: 2 x 128 accumulator + 4 x 64 A columns
+    p.stages = stages > cap ? cap : stages;
+    if (p.stages < 2) {
+        cg_set_error("k_gemm_tc: stage does not fit shared memory");
+        return -1;
+    }
+    const size_t smem = (size_t)p.stages * stage_bytes + SMEM_FIXED;
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)(4 * STAGE_BYTES_1X + 1024 + 1024 + EPI_BYTES));
+                                             SMEM_LIMIT);
         if (e != cudaSuccess) return cg_cuda_fail(e, "cudaFuncSetAttribute(k_gemm_tc)");
         attr_set = true;
     }
@@ -476,13 +776,16 @@ int launch(const Params &p0, const CUtensorMap &a0, const CUtensorMap &b0, const
     }
     const int64_t tiles = (int64_t)((p.N + p.BN - 1) / p.BN) * ((p.M + BM - 1) / BM) * grid_z;
     const unsigned grid = (unsigned)(tiles < n_sm ? tiles : n_sm);   // persistent
-    k_gemm_tc<<<grid, THREADS, smem, st>>>(a0, b0, a1, b1, p);
+    k_gemm_tc<<<grid, THREADS, smem, st>>>(a0, b0, a1, b1, bl0, bl1, mc, p);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 1 : cg_cuda_fail(e, "k_gemm_tc");
 }
 
-inline int bn_for(int N) {
-    int bn = N < BN_MAX ? ((N + 15) / 16) * 16 : BN_MAX;
+inline int bn_for(int N, bool split3) {
+    const int cap = split3 ? BN_MAX_3X : BN_MAX;
+    // equal-width n tiles (e.g. N = 256 -> 2 x 128 under 3xTF32)
+    const int n_tiles = (N + cap - 1) / cap;
+    int bn = ((N + n_tiles - 1) / n_tiles + 15) / 16 * 16;
     return bn < 16 ? 16 : bn;
 }
 
@@ -493,7 +796,7 @@ inline int bn_for(int N) {
 int cg_gemm_tc(int64_t M, int N, int K1, const float *A1, int64_t lda1, const float *B1, int K2,
                const float *A2, int64_t lda2, const float *B2, int trans_b, const float *bias,
                int relu, const float *row_scale, const float *mask, int64_t ldm, float *C,
-               int64_t ldc, int mode, cudaStream_t st) {
+               int64_t ldc, int mode, const float *B1_lo, const float *B2_lo, cudaStream_t st) {
     using namespace tc;
     if (mode != 1 && mode != 2) {
         cg_set_error("cg_gemm: unknown mode");
@@ -507,8 +810,8 @@ int cg_gemm_tc(int64_t M, int N, int K1, const float *A1, int64_t lda1, const fl
     Params p{};
     p.M = M;
     p.N = N;
-    p.BN = bn_for(N);
     p.split3 = mode == 1;
+    p.BN = bn_for(N, p.split3);
     p.bias = bias;
     p.relu = relu;
     p.row_scale = row_scale;
@@ -517,12 +820,16 @@ int cg_gemm_tc(int64_t M, int N, int K1, const float *A1, int64_t lda1, const fl
     p.C = C;
     p.ldc = ldc;
     p.k_chunk = 0;
-    CUtensorMap ma[2], mb[2];
+    p.vec_ok = !(ldc % 4) && !((uintptr_t)C % 16) && (!mask || (!(ldm % 4) && !((uintptr_t)mask % 16))) &&
+               (!bias || !((uintptr_t)bias % 16));
+    CUtensorMap ma[2], mb[2], mbl[2];
     const float *As[2] = {A1, A2};
     const float *Bs[2] = {B1, B2};
+    const float *Bls[2] = {B1_lo, B2_lo};
     const int Ks[2] = {K1, K2};
     const int64_t ldas[2] = {lda1, lda2};
     p.n_ops = (A2 && K2 > 0) ? 2 : 1;
+    p.b_presplit = p.split3 && B1_lo && (p.n_ops == 1 || B2_lo);
     for (int o = 0; o < p.n_ops; ++o) {
         p.op[o].K = Ks[o];
         p.op[o].a_mn = 0;
@@ -530,6 +837,11 @@ int cg_gemm_tc(int64_t M, int N, int K1, const float *A1, int64_t lda1, const fl
         bool ok = make_map(&ma[o], As[o], Ks[o], M, ldas[o], BM, false);
         ok = ok && (trans_b ? make_map(&mb[o], Bs[o], Ks[o], N, Ks[o], p.BN, false)
                             : make_map(&mb[o], Bs[o], N, Ks[o], N, 32, true));
+        if (p.b_presplit)
+            ok = ok && (trans_b ? make_map(&mbl[o], Bls[o], Ks[o], N, Ks[o], p.BN, false)
+                                : make_map(&mbl[o], Bls[o], N, Ks[o], N, 32, true));
+        else
+            mbl[o] = mb[o];
         if (!ok) {
             cg_set_error("cg_gemm_tc: cuTensorMapEncodeTiled failed");
             return -1;
@@ -538,8 +850,9 @@ int cg_gemm_tc(int64_t M, int N, int K1, const float *A1, int64_t lda1, const fl
     if (p.n_ops == 1) {
         ma[1] = ma[0];
         mb[1] = mb[0];
+        mbl[1] = mbl[0];
     }
-    return launch(p, ma[0], mb[0], ma[1], mb[1], 1, st);
+    return launch(p, ma[0], mb[0], ma[1], mb[1], mbl[0], mbl[1], 1, st);
 }
 
 // Partial weight gradients: ws[c][k][n] = sum_{m in chunk c} A[m, k] D[m, n].
@@ -553,8 +866,8 @@ int cg_wgrad_tc(int64_t M, int K, int N, const float *A, int64_t lda, const floa
     Params p{};
     p.M = K;          // output rows = input features
     p.N = N;
-    p.BN = bn_for(N);
     p.split3 = mode == 1;
+    p.BN = bn_for(N, p.split3);
     p.n_ops = 1;
     p.op[0].K = (int)M;  // reduction over vertices
     p.op[0].a_mn = 1;
@@ -562,10 +875,11 @@ int cg_wgrad_tc(int64_t M, int K, int N, const float *A, int64_t lda, const floa
     p.k_chunk = chunk;
     p.C = ws;
     p.ldc = N;
+    p.vec_ok = !(N % 4) && !((uintptr_t)ws % 16);
     CUtensorMap ma, mb;
     if (!make_map(&ma, A, K, M, lda, BK, true) || !make_map(&mb, D, N, M, ldd, BK, true)) {
         cg_set_error("cg_wgrad_tc: cuTensorMapEncodeTiled failed");
         return -1;
     }
-    return launch(p, ma, mb, ma, mb, (int)n_chunks, st);
+    return launch(p, ma, mb, ma, mb, mb, mb, (int)n_chunks, st);
 }

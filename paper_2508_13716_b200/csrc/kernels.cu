@@ -344,9 +344,15 @@ __global__ void k_scale_rows_to(float *__restrict__ dst, int64_t ldd, const floa
     }
 }
 
+__device__ __forceinline__ void split_tf32(float x, float &hi, float &lo) {
+    hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+    lo = x - hi;
+}
+
 __global__ void k_adam(int64_t n, float *__restrict__ p, const float *__restrict__ g,
                        float *__restrict__ m, float *__restrict__ v, float lr, float b1,
-                       float b2, float eps, float c1, float c2) {
+                       float b2, float eps, float c1, float c2, float *__restrict__ p_hi,
+                       float *__restrict__ p_lo) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         float gi = g[i];
@@ -354,7 +360,41 @@ __global__ void k_adam(int64_t n, float *__restrict__ p, const float *__restrict
         float vi = b2 * v[i] + (1.f - b2) * gi * gi;
         m[i] = mi;
         v[i] = vi;
-        p[i] -= lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+        const float pi = p[i] - lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+        p[i] = pi;
+        if (p_hi) {
+            float h, l;
+            split_tf32(pi, h, l);
+            p_hi[i] = h;
+            p_lo[i] = l;
+        }
+    }
+}
+
+// blockIdx.y = matrix; element e = i * cols + j of matrix m goes to j * rows + i
+__global__ void k_split_tf32_t(const int64_t *__restrict__ off, const int32_t *__restrict__ rows,
+                               const int32_t *__restrict__ cols, const float *__restrict__ x,
+                               float *__restrict__ hi, float *__restrict__ lo) {
+    const int m = blockIdx.y;
+    const int64_t o = off[m];
+    const int r = rows[m], c = cols[m];
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= (int64_t)r * c) return;
+    const int i = (int)(e / c), j = (int)(e % c);
+    float h, l;
+    split_tf32(x[o + e], h, l);
+    hi[o + (int64_t)j * r + i] = h;
+    lo[o + (int64_t)j * r + i] = l;
+}
+
+__global__ void k_split_tf32(int64_t n, const float *__restrict__ x, float *__restrict__ hi,
+                             float *__restrict__ lo) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float h, l;
+        split_tf32(x[i], h, l);
+        hi[i] = h;
+        lo[i] = l;
     }
 }
 
@@ -583,13 +623,34 @@ int cg_softmax_ce(int64_t n_rows, int C, const float *logits, int64_t ld, const 
 }
 
 int cg_adam(int64_t n, float *param, const float *grad, float *m, float *v, float lr,
-            float beta1, float beta2, float eps, int step, void *stream) {
+            float beta1, float beta2, float eps, int step, float *p_hi, float *p_lo,
+            void *stream) {
     if (n == 0) return 0;
+    if ((p_hi == nullptr) != (p_lo == nullptr)) {
+        cg_set_error("cg_adam: p_hi and p_lo must both be set or both be NULL");
+        return -1;
+    }
     double c1 = 1.0 - pow((double)beta1, (double)step);
     double c2 = 1.0 - pow((double)beta2, (double)step);
     k_adam<<<grid_for(n, 256, 148 * 8), 256, 0, (cudaStream_t)stream>>>(
-        n, param, grad, m, v, lr, beta1, beta2, eps, (float)c1, (float)c2);
+        n, param, grad, m, v, lr, beta1, beta2, eps, (float)c1, (float)c2, p_hi, p_lo);
     CG_CHECK_LAUNCH("k_adam");
+    return 1;
+}
+
+int cg_split_tf32_t(int n_mats, const int64_t *off, const int32_t *rows, const int32_t *cols,
+                    const float *x, float *hi, float *lo, int64_t max_elems, void *stream) {
+    if (n_mats == 0 || max_elems == 0) return 0;
+    dim3 grid((unsigned)((max_elems + 255) / 256), (unsigned)n_mats);
+    k_split_tf32_t<<<grid, 256, 0, (cudaStream_t)stream>>>(off, rows, cols, x, hi, lo);
+    CG_CHECK_LAUNCH("k_split_tf32_t");
+    return 1;
+}
+
+int cg_split_tf32(int64_t n, const float *x, float *hi, float *lo, void *stream) {
+    if (n == 0) return 0;
+    k_split_tf32<<<grid_for(n, 256, 148 * 8), 256, 0, (cudaStream_t)stream>>>(n, x, hi, lo);
+    CG_CHECK_LAUNCH("k_split_tf32");
     return 1;
 }
 

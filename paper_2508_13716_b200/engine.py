@@ -83,7 +83,12 @@ class Engine:
         self.dY = [torch.zeros(D.n_in, wmax, dtype=f32, device=dev) for _ in range(2)]
         fmax_b = max(self.F[1:], default=4)
         n_bwd = D.bwd_stage_vertex.size
-        self.G = torch.zeros(D.n_in + n_bwd, fmax_b, dtype=f32, device=dev)
+        # backward gradient rows [inner | staged remote rows], double-buffered
+        # by layer parity when peers pull from it: a rank may overwrite its
+        # layer-(l-1) rows while a slower peer still pulls its layer-l rows
+        # (the next barrier orders the reuse two layers later)
+        G0 = torch.zeros(D.n_in + n_bwd, fmax_b, dtype=f32, device=dev)
+        self.Gs = [G0, torch.zeros_like(G0) if self.comm.world > 1 else G0]
         self.Hs = torch.zeros(D.n_in, fmax_b, dtype=f32, device=dev) if self.kind == "sage" else None
         # parameters (flat) + grads (+1 slot for the loss) + Adam state
         self.pshapes = []
@@ -108,6 +113,23 @@ class Engine:
             flat[self.poff[i]:self.poff[i] + sizes[i]] = p.ravel()
         self.psizes = sizes
         self.params = _dev(flat, f32, dev)
+        if self.gemm_mode == 1:
+            # 3xTF32: weights kept pre-split for the GEMM B operand, plus a
+            # transposed copy so the forward transform reads W K-major too
+            self.params_hi = torch.empty_like(self.params)
+            self.params_lo = torch.empty_like(self.params)
+            self.paramsT_hi = torch.zeros_like(self.params)
+            self.paramsT_lo = torch.zeros_like(self.params)
+            mats = [i for i, sh in enumerate(self.pshapes) if len(sh) == 2]
+            self._wt_tab = (_dev([int(self.poff[i]) for i in mats], torch.int64, dev),
+                            _dev([self.pshapes[i][0] for i in mats], torch.int32, dev),
+                            _dev([self.pshapes[i][1] for i in mats], torch.int32, dev),
+                            len(mats), max(int(np.prod(self.pshapes[i])) for i in mats))
+            call("cg_split_tf32", self.n_params, ptr(self.params), ptr(self.params_hi),
+                 ptr(self.params_lo), self.stream())
+            self._split_t()
+        else:
+            self.params_hi = self.params_lo = None
         self.grads = torch.zeros(self.n_params + 1, dtype=f32, device=dev)
         self.adam_m = torch.zeros(self.n_params, dtype=f32, device=dev)
         self.adam_v = torch.zeros(self.n_params, dtype=f32, device=dev)
@@ -164,8 +186,10 @@ class Engine:
             self.tab.append(_dev(np.array(peers + [self.host.ptr + 4 * int(self.layer_off[l])],
                                           np.uint64).view(np.int64), torch.int64, dev))
             self.tab_ld.append(_dev(np.array([F] * nd + [self.bpe_f], np.int64), i64, dev))
-        gpeers = self.comm.exchange_pointers(ptr(self.G), self.dev.index)
-        self.tabG = _dev(np.array(gpeers, np.uint64).view(np.int64), torch.int64, dev)
+        self.tabGs = []
+        for Gb in self.Gs:
+            gpeers = self.comm.exchange_pointers(ptr(Gb), self.dev.index)
+            self.tabGs.append(_dev(np.array(gpeers, np.uint64).view(np.int64), torch.int64, dev))
         self._tabG_lds = {}
         # aggregated narrow gradients (backward aggregate-then-transform layers)
         self.T = torch.zeros(D.n_in, max(self.dims[1:]), dtype=f32, device=dev)
@@ -195,6 +219,31 @@ class Engine:
 
     def _p(self, i: int) -> int:
         return ptr(self.params) + 4 * int(self.poff[i])
+
+    def _split_t(self):
+        off, rows, cols, n, mx = self._wt_tab
+        call("cg_split_tf32_t", n, ptr(off), ptr(rows), ptr(cols), ptr(self.params),
+             ptr(self.paramsT_hi), ptr(self.paramsT_lo), mx, self.stream())
+
+    def _gemm(self, M, N, K1, A1, lda1, w1, K2=0, A2=None, lda2=0, w2=None, *, trans_b,
+              bias=None, relu=0, row_scale=None, mask=None, ldm=0, C, ldc):
+        """cg_gemm with weight operands given as parameter indices: under
+        3xTF32 the weights are read pre-split (params_hi / params_lo, kept
+        current by cg_adam), so the kernel splits only the activations."""
+        split = self.params_hi is not None
+        def b(i, arr):
+            return None if i is None else ptr(arr) + 4 * int(self.poff[i])
+        if split and trans_b == 0:   # W [K x N] -> its transpose, K-major
+            B1, B2 = b(w1, self.paramsT_hi), b(w2, self.paramsT_hi)
+            L1, L2 = b(w1, self.paramsT_lo), b(w2, self.paramsT_lo)
+            trans_b = 1
+        elif split:
+            B1, B2 = b(w1, self.params_hi), b(w2, self.params_hi)
+            L1, L2 = b(w1, self.params_lo), b(w2, self.params_lo)
+        else:
+            B1, B2, L1, L2 = b(w1, self.params), b(w2, self.params), None, None
+        call("cg_gemm", M, N, K1, A1, lda1, B1, K2, A2, lda2, B2, trans_b, bias, relu,
+             row_scale, mask, ldm, C, ldc, self.gemm_mode, L1, L2, self.stream())
 
     def _g(self, i: int) -> int:
         return ptr(self.grads) + 4 * int(self.poff[i])
@@ -395,14 +444,13 @@ class Engine:
             last = l == nL - 1
             out = self.logits if last else self.X[l + 1]
             if kind == "gcn":
-                call("cg_gemm", n_in, Fo, F, ptr(self.Z[l]), F, self._p(2 * l), 0, None, 0, None,
-                     0, self._p(2 * l + 1), 0 if last else 1,
-                     None if last else ptr(self.norm_src), None, 0, ptr(out), Fo,
-                     self.gemm_mode, st)
+                self._gemm(n_in, Fo, F, ptr(self.Z[l]), F, 2 * l, trans_b=0,
+                           bias=self._p(2 * l + 1), relu=0 if last else 1,
+                           row_scale=None if last else ptr(self.norm_src), C=ptr(out), ldc=Fo)
             else:
-                call("cg_gemm", n_in, Fo, F, ptr(self.X[l]), F, self._p(3 * l), F,
-                     ptr(self.Z[l]), F, self._p(3 * l + 1), 0, self._p(3 * l + 2),
-                     0 if last else 1, None, None, 0, ptr(out), Fo, self.gemm_mode, st)
+                self._gemm(n_in, Fo, F, ptr(self.X[l]), F, 3 * l, F, ptr(self.Z[l]), F,
+                           3 * l + 1, trans_b=0, bias=self._p(3 * l + 2),
+                           relu=0 if last else 1, C=ptr(out), ldc=Fo)
         # ---------------- loss
         n_total = self.L.n
         loss_ptr = ptr(self.grads) + 4 * self.n_params
@@ -427,37 +475,37 @@ class Engine:
                 break
             nxt = self.dY[1 - cur] if l != nL - 1 else self.dY[cur]
             wide = Fo < F  # aggregate the narrower gradient, then transform
+            G = self.Gs[l & 1]
             W = 2 * l if kind == "gcn" else 3 * l + 1
             if wide:
                 # G = (b | 1/d_in) * dY  (F_out wide): the rows peers pull
-                call("cg_scale_rows_to", ptr(self.G), Fo, ptr(dY), Fo, n_in, Fo,
+                call("cg_scale_rows_to", ptr(G), Fo, ptr(dY), Fo, n_in, Fo,
                      ptr(self.norm_dst), st)
                 Fx = Fo
             elif kind == "gcn":
-                call("cg_gemm", n_in, F, Fo, ptr(dY), Fo, self._p(W), 0, None, 0, None, 1,
-                     None, 0, ptr(self.norm_dst), None, 0, ptr(self.G), F, self.gemm_mode, st)
+                self._gemm(n_in, F, Fo, ptr(dY), Fo, W, trans_b=1, row_scale=ptr(self.norm_dst),
+                           C=ptr(G), ldc=F)
                 Fx = F
             else:
-                call("cg_gemm", n_in, F, Fo, ptr(dY), Fo, self._p(W), 0, None, 0, None,
-                     1, None, 0, ptr(self.norm_dst), None, 0, ptr(self.G), F, self.gemm_mode, st)
-                call("cg_gemm", n_in, F, Fo, ptr(dY), Fo, self._p(3 * l), 0, None, 0, None, 1,
-                     None, 0, None, None, 0, ptr(self.Hs), F, self.gemm_mode, st)
+                self._gemm(n_in, F, Fo, ptr(dY), Fo, W, trans_b=1, row_scale=ptr(self.norm_dst),
+                           C=ptr(G), ldc=F)
+                self._gemm(n_in, F, Fo, ptr(dY), Fo, 3 * l, trans_b=1, C=ptr(self.Hs), ldc=F)
                 Fx = F
             self.comm.barrier()
             if self.n_bwd:
-                self._copy(self.n_bwd, Fx, self.b_src, self.b_row, self.b_dst, self.tabG,
-                           self._tabG_ld(Fx), self.G, Fx)
+                self._copy(self.n_bwd, Fx, self.b_src, self.b_row, self.b_dst, self.tabGs[l & 1],
+                           self._tabG_ld(Fx), G, Fx)
             if timers:
                 a, b = mk(), mk()
                 a.record()
             if wide:
                 # T = (a | 1) * A^T G, then dY_{l-1} = mask * (T W^T [+ dY W_self^T])
                 call("cg_spmm", n_in, Fx, ptr(self.bwd_rowptr), ptr(self.bwd_col), 1 << 62, None,
-                     ptr(self.G), Fx, ptr(self.norm_src) if kind == "gcn" else None, None, 0,
+                     ptr(G), Fx, ptr(self.norm_src) if kind == "gcn" else None, None, 0,
                      None, 0, ptr(self.T), Fx, st)
             else:
                 call("cg_spmm", n_in, F, ptr(self.bwd_rowptr), ptr(self.bwd_col), 1 << 62, None,
-                     ptr(self.G), F, ptr(self.norm_src) if kind == "gcn" else None,
+                     ptr(G), F, ptr(self.norm_src) if kind == "gcn" else None,
                      ptr(self.Hs) if kind == "sage" else None, F, ptr(self.X[l]), F, ptr(nxt), F,
                      st)
             if timers:
@@ -465,12 +513,11 @@ class Engine:
                 bwd_ev.append((a, b))
             if wide:
                 if kind == "gcn":
-                    call("cg_gemm", n_in, F, Fo, ptr(self.T), Fo, self._p(W), 0, None, 0, None, 1,
-                         None, 0, None, ptr(self.X[l]), F, ptr(nxt), F, self.gemm_mode, st)
+                    self._gemm(n_in, F, Fo, ptr(self.T), Fo, W, trans_b=1, mask=ptr(self.X[l]),
+                               ldm=F, C=ptr(nxt), ldc=F)
                 else:
-                    call("cg_gemm", n_in, F, Fo, ptr(dY), Fo, self._p(3 * l), Fo, ptr(self.T), Fo,
-                         self._p(W), 1, None, 0, None, ptr(self.X[l]), F, ptr(nxt), F,
-                         self.gemm_mode, st)
+                    self._gemm(n_in, F, Fo, ptr(dY), Fo, 3 * l, Fo, ptr(self.T), Fo, W,
+                               trans_b=1, mask=ptr(self.X[l]), ldm=F, C=ptr(nxt), ldc=F)
             if l != nL - 1:
                 cur = 1 - cur
         # ---------------- K7 + optimizer
@@ -478,7 +525,11 @@ class Engine:
         self._gw(nL - 1)
         self.step += 1
         call("cg_adam", self.n_params, ptr(self.params), ptr(self.grads), ptr(self.adam_m),
-             ptr(self.adam_v), self.lr, 0.9, 0.999, 1e-8, self.step, st)
+             ptr(self.adam_v), self.lr, 0.9, 0.999, 1e-8, self.step,
+             ptr(self.params_hi) if self.params_hi is not None else None,
+             ptr(self.params_lo) if self.params_lo is not None else None, st)
+        if self.params_hi is not None:
+            self._split_t()
         if timers:
             t1 = mk()
             t1.record()

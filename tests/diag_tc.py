@@ -12,7 +12,7 @@ def run(M, N, K, tb, mode, seed=0):
     ref = A.astype(np.float64) @ (B.T if tb else B)
     out = torch.full((M, N), float("nan"), device="cuda")
     tA, tB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
-    call("cg_gemm", M, N, K, ptr(tA), K, ptr(tB), 0, None, 0, None, tb, None, 0, None, None, 0, ptr(out), N, mode,
+    call("cg_gemm", M, N, K, ptr(tA), K, ptr(tB), 0, None, 0, None, tb, None, 0, None, None, 0, ptr(out), N, mode, None, None,
          torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     got = out.cpu().numpy()
