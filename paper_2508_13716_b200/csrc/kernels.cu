@@ -114,10 +114,16 @@ __global__ void k_copy_rows(int64_t n, int F, const int32_t *__restrict__ src_id
 // ---------------------------------------------------------------- K1 ------
 
 // G lanes per row, NCH float4 chunks per lane (row width F <= 4*G*NCH).
-// Column indices are loaded G at a time (coalesced), the halo indirection
-// (cache lookup -> slab / staging / owner row) is resolved per lane, then
-// broadcast with shuffles; UNR row gathers are in flight per lane.  The
-// accumulation order is the CSR order.
+// Each G-lane group walks rows r, r+ngrp, ... through a 4-stage software
+// pipeline so the index chase never sits in front of the gathers:
+//   A  rowptr of row k+3      B  first G column ids of row k+2
+//   C  cache lookup (halo_row indirection: slab slot / staging row / owner
+//      row) of row k+1        D  the row-k gathers: UNR rows of 128-bit loads
+//                                in flight per lane, CSR-order accumulation.
+// Loads issued in stages A-C are consumed one iteration later, behind the
+// gathers of the current row.  Rows with more than G edges finish their tail
+// inline.  The grid is sized to the resident-block count (persistent), so a
+// group sees many rows and the pipeline stays full.
 template <int G, int NCH>
 __global__ void __launch_bounds__(256)
 k_spmm(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
@@ -130,71 +136,88 @@ k_spmm(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
     const unsigned gmask = (G == 32) ? 0xffffffffu
                                      : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
     const int nchunk = F >> 2;
-    int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
-    int64_t ngrp = (int64_t)gridDim.x * blockDim.x / G;
-    for (int64_t r = grp; r < n_rows; r += ngrp) {
+    const int64_t ngrp = (int64_t)gridDim.x * blockDim.x / G;
+    int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+
+    auto lookup = [&](int32_t c) -> int64_t {
+        return (c < n_direct || halo_row == nullptr) ? (int64_t)c : (int64_t)halo_row[c - n_direct];
+    };
+    auto gather_add = [&](int64_t src, float4 (&acc)[NCH]) {
+        const float4 *p = reinterpret_cast<const float4 *>(X + src * ldx);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            const int ch = lane + c * G;
+            if (ch < nchunk) {
+                const float4 t = __ldg(p + ch);
+                acc[c].x += t.x; acc[c].y += t.y; acc[c].z += t.z; acc[c].w += t.w;
+            }
+        }
+    };
+
+    // pipeline prologue: rows k, k+1, k+2 (r1, r2, r3 = r + ngrp, ...)
+    int64_t b0 = 0, e0 = 0, b1 = 0, e1 = 0, b2 = 0, e2 = 0;
+    if (r < n_rows) { b0 = rowptr[r]; e0 = rowptr[r + 1]; }
+    if (r + ngrp < n_rows) { b1 = rowptr[r + ngrp]; e1 = rowptr[r + ngrp + 1]; }
+    if (r + 2 * ngrp < n_rows) { b2 = rowptr[r + 2 * ngrp]; e2 = rowptr[r + 2 * ngrp + 1]; }
+    int32_t c1 = (lane < e1 - b1) ? col[b1 + lane] : 0;
+    int64_t s0 = (lane < e0 - b0) ? lookup(col[b0 + lane]) : 0;
+
+    for (; r < n_rows; r += ngrp) {
+        // A: rowptr of row k+3
+        const int64_t r3 = r + 3 * ngrp;
+        int64_t b3 = 0, e3 = 0;
+        if (r3 < n_rows) { b3 = rowptr[r3]; e3 = rowptr[r3 + 1]; }
+        // B: column ids of row k+2
+        const int32_t c2 = (lane < e2 - b2) ? col[b2 + lane] : 0;
+        // C: cache lookup of row k+1
+        const int64_t s1 = (lane < e1 - b1) ? lookup(c1) : 0;
+        // D: gathers of row k
         float4 acc[NCH];
 #pragma unroll
         for (int c = 0; c < NCH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-        const int64_t e0 = rowptr[r], e1 = rowptr[r + 1];
-        for (int64_t eb = e0; eb < e1; eb += G) {
-            const int cnt = (int)((e1 - eb) < (int64_t)G ? (e1 - eb) : (int64_t)G);
-            int64_t myrow = 0;
-            if (lane < cnt) {
-                int64_t c = col[eb + lane];
-                myrow = (c < n_direct || halo_row == nullptr) ? c : halo_row[c - n_direct];
-            }
-            int j = 0;
-            for (; j + UNR <= cnt; j += UNR) {
-                float4 v[UNR][NCH];
+        const int cnt = (int)((e0 - b0) < (int64_t)G ? (e0 - b0) : (int64_t)G);
+        int j = 0;
+        for (; j + UNR <= cnt; j += UNR) {
+            float4 v[UNR][NCH];
 #pragma unroll
-                for (int u = 0; u < UNR; ++u) {
-                    int64_t rr = __shfl_sync(gmask, myrow, j + u, G);
-                    const float4 *src = reinterpret_cast<const float4 *>(X + rr * ldx);
-#pragma unroll
-                    for (int c = 0; c < NCH; ++c) {
-                        int ch = lane + c * G;
-                        v[u][c] = ch < nchunk ? __ldg(src + ch) : make_float4(0.f, 0.f, 0.f, 0.f);
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < UNR; ++u)
-#pragma unroll
-                    for (int c = 0; c < NCH; ++c) {
-                        acc[c].x += v[u][c].x;
-                        acc[c].y += v[u][c].y;
-                        acc[c].z += v[u][c].z;
-                        acc[c].w += v[u][c].w;
-                    }
-            }
-            for (; j < cnt; ++j) {
-                int64_t rr = __shfl_sync(gmask, myrow, j, G);
+            for (int u = 0; u < UNR; ++u) {
+                const int64_t rr = __shfl_sync(gmask, s0, j + u, G);
                 const float4 *src = reinterpret_cast<const float4 *>(X + rr * ldx);
 #pragma unroll
                 for (int c = 0; c < NCH; ++c) {
-                    int ch = lane + c * G;
-                    if (ch < nchunk) {
-                        float4 t = __ldg(src + ch);
-                        acc[c].x += t.x;
-                        acc[c].y += t.y;
-                        acc[c].z += t.z;
-                        acc[c].w += t.w;
-                    }
+                    const int ch = lane + c * G;
+                    v[u][c] = ch < nchunk ? __ldg(src + ch) : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u)
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) {
+                    acc[c].x += v[u][c].x;
+                    acc[c].y += v[u][c].y;
+                    acc[c].z += v[u][c].z;
+                    acc[c].w += v[u][c].w;
+                }
         }
-        const float s = scale ? scale[r] : 1.0f;
+        for (; j < cnt; ++j) gather_add(__shfl_sync(gmask, s0, j, G), acc);
+        // tail of a row with more than G edges (rare): inline, same order
+        for (int64_t eb = b0 + G; eb < e0; eb += G) {
+            const int n2 = (int)((e0 - eb) < (int64_t)G ? (e0 - eb) : (int64_t)G);
+            const int64_t sx = (lane < n2) ? lookup(col[eb + lane]) : 0;
+            for (int t = 0; t < n2; ++t) gather_add(__shfl_sync(gmask, sx, t, G), acc);
+        }
+        const float sc = scale ? scale[r] : 1.0f;
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
-            int ch = lane + c * G;
+            const int ch = lane + c * G;
             if (ch >= nchunk) continue;
-            float4 o = make_float4(acc[c].x * s, acc[c].y * s, acc[c].z * s, acc[c].w * s);
+            float4 o = make_float4(acc[c].x * sc, acc[c].y * sc, acc[c].z * sc, acc[c].w * sc);
             if (addend) {
-                float4 a = reinterpret_cast<const float4 *>(addend + r * ld_add)[ch];
+                const float4 a = reinterpret_cast<const float4 *>(addend + r * ld_add)[ch];
                 o.x += a.x; o.y += a.y; o.z += a.z; o.w += a.w;
             }
             if (mask) {
-                float4 m = reinterpret_cast<const float4 *>(mask + r * ld_mask)[ch];
+                const float4 m = reinterpret_cast<const float4 *>(mask + r * ld_mask)[ch];
                 o.x = m.x > 0.f ? o.x : 0.f;
                 o.y = m.y > 0.f ? o.y : 0.f;
                 o.z = m.z > 0.f ? o.z : 0.f;
@@ -202,6 +225,10 @@ k_spmm(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
             }
             reinterpret_cast<float4 *>(out + r * ldo)[ch] = o;
         }
+        // rotate the pipeline
+        b0 = b1; e0 = e1; s0 = s1;
+        b1 = b2; e1 = e2; c1 = c2;
+        b2 = b3; e2 = e3;
     }
 }
 
@@ -501,6 +528,17 @@ k_plan_frozen(cg_plan_static st, int e, int s, int me, int32_t *req_ver,
                                 (unsigned long long)tally[i]);
 }
 
+inline int n_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
 inline int grid_for(int64_t work, int threads, int max_blocks = 148 * 16) {
     int64_t b = (work + threads - 1) / threads;
     if (b < 1) b = 1;
@@ -562,9 +600,17 @@ int cg_spmm(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col, in
     const int threads = 256;
     cudaStream_t st = (cudaStream_t)stream;
 #define CG_SPMM_LAUNCH(G, NCH)                                                              \
-    k_spmm<G, NCH><<<grid_for(n_rows * G, threads, 148 * 64), threads, 0, st>>>(           \
-        n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, scale, addend, ld_add, mask, \
-        ld_mask, out, ldo)
+    do {                                                                                    \
+        static int blocks_per_sm = 0;                                                       \
+        if (!blocks_per_sm) {                                                               \
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_spmm<G, NCH>,   \
+                                                          threads, 0);                      \
+            if (blocks_per_sm < 1) blocks_per_sm = 1;                                       \
+        }                                                                                   \
+        k_spmm<G, NCH><<<grid_for(n_rows * G, threads, n_sms() * blocks_per_sm), threads, 0, \
+                         st>>>(n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, scale,  \
+                               addend, ld_add, mask, ld_mask, out, ldo);                    \
+    } while (0)
     if (nchunk <= 8) CG_SPMM_LAUNCH(8, 1);
     else if (nchunk <= 16) CG_SPMM_LAUNCH(16, 1);
     else if (nchunk <= 32) CG_SPMM_LAUNCH(32, 1);
