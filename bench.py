@@ -113,11 +113,6 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
     from paper_2508_13716_b200 import _lib, api, hostgraph as H
-    from paper_2508_13716_b200.engine import Engine
-    from paper_2508_13716_b200.comm import DistComm, SoloComm
-    from paper_2508_13716_b200.layout import build_layout
-    from paper_2508_13716_b200.models import init_params
-    from paper_2508_13716_b200.planner import SequentialPlanner
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -125,20 +120,16 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    comm = DistComm(local) if world > 1 else SoloComm()
     t_setup = time.perf_counter()
     g, ps, caps = build_workload(args.parts)
-    union, score = H.influence_scores(g, ps)
-    ranked = [h[np.lexsort((h, -score[np.searchsorted(union, h)]))] for h in ps.halo]
-    planner = SequentialPlanner("jaca", caps.c_cpu, caps.c_gpu, union, score, ps.halo, ranked)
-    planner.warm()
-    layout = build_layout(g, ps.inner, ps.halo, caps.c_gpu, world, "gcn")
-    dims = list(F_DIM) + [CLASSES]
-    eng = Engine(layout, rank, "gcn", dims, H.feature_bytes(F_DIM), caps, planner,
-                 args.staleness, "jaca", comm=comm, gemm=args.gemm,
-                 params_init=init_params("gcn", dims, 2), device=local)
+    cfg = H.SimConfig(epochs=args.warmup + args.steps, policy="jaca",
+                      staleness_bound=args.staleness, f_dim=F_DIM, L=len(F_DIM))
+    # the public drop-in, stepwise: same setup as api.train()
+    sess = api.TrainSession(g, ps, H.unit_profiles(args.parts), caps, cfg, model="gcn",
+                            num_classes=CLASSES, gemm=args.gemm, keep_logits="none")
+    eng = sess.engine
     t_setup = time.perf_counter() - t_setup
-    D = layout.devices[rank]
+    D = eng.D
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -146,10 +137,9 @@ def run_ours(args):
             dist.barrier()
 
     # warm-up (includes the host-planned transient epoch and the warm fill)
-    e = 0
     for _ in range(args.warmup):
-        e += 1
-        eng.finish(eng.run_epoch(e, timers=True, sync=False))
+        sess.step(sync=False)
+    sess.finish()
     # ---- device-timed region: K epochs, inputs resident in HBM
     barrier()
     torch.cuda.synchronize()
@@ -160,13 +150,12 @@ def run_ours(args):
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         for _ in range(args.steps):
-            e += 1
-            stats.append(eng.run_epoch(e, timers=True, sync=False))
+            stats.append(sess.step(sync=False))
         t1.record(stream)
         torch.cuda.synchronize()
     barrier()
     launches = _lib.launches["total"] - launches0
-    stats = [eng.finish(s) for s in stats]
+    sess.finish()   # completes (in place) the EpochStats of the timed epochs
     dev_ms = t0.elapsed_time(t1)
     if world > 1:
         t = torch.tensor([dev_ms], device="cuda")
@@ -201,39 +190,54 @@ def run_ours(args):
     fwd_uncached = int(sum(h.size for h in ps.halo)) * bpe
     bwd_model = int(sum(ps.cut_edges)) * bpe
 
-    # ---- end-to-end: the same epochs with host buffers, copies inside the timed region
+    # ---- end-to-end through the public session API: every step uploads its
+    # input rows from pinned host memory (H2D) and downloads its logits and
+    # loss (D2H).  Uploads run one step ahead on a copy stream and downloads
+    # overlap the backward pass; the clock is the host wall clock around the
+    # whole run including the final synchronisation.
     from paper_2508_13716_b200.models import _unit  # deterministic host features
     rows = D.verts.astype(np.uint64)[:, None]
     host_x = torch.from_numpy(_unit(0, rows, np.arange(F_DIM[0], dtype=np.uint64)[None, :])).pin_memory()
-    host_logits = torch.empty(D.n_in, eng.C4).pin_memory()
-    host_loss = torch.empty(1).pin_memory()
+    e2e_steps = args.steps
+    host_logits = [torch.empty(D.n_in, eng.C4).pin_memory() for _ in range(2)]
+    host_loss = torch.empty(e2e_steps + 2).pin_memory()
+
+    def e2e_run(n, loss_off):
+        sess.prefetch_features(host_x)
+        for i in range(n):
+            s = sess.step(sync=False)
+            if i + 1 < n:
+                sess.prefetch_features(host_x)      # next step's inputs, behind this epoch
+            sess.fetch_logits(host_logits[i & 1])
+            sess.fetch_loss(s, host_loss[loss_off + i:loss_off + i + 1])
+
+    e2e_run(2, e2e_steps)        # warm-up: copy streams, staging buffer, pinned paths
+    torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
-    e2e_steps = max(2, args.steps // 2)
     w0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        e += 1
-        eng.upload_features(host_x)
-        s = eng.run_epoch(e, timers=False, sync=False)
-        host_loss.copy_(s.loss, non_blocking=True)
-        host_logits.copy_(eng.logits, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+    e2e_run(e2e_steps, 0)
+    torch.cuda.synchronize()
     barrier()
     w_s = time.perf_counter() - w0
+    sess.finish()
     if world > 1:
         t = torch.tensor([w_s], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         w_s = float(t.item())
     e2e = {"value": L * E * e2e_steps / w_s / 1e9, "unit": "GTEPS",
            "h2d_bytes_per_step": int(host_x.numel() * 4),
-           "d2h_bytes_per_step": int(host_logits.numel() * 4 + 4),
-           "how": "per epoch: pinned-host features H2D (+ GCN row scaling), epoch, loss + "
-                  "logits D2H, host wall clock incl. sync"}
+           "d2h_bytes_per_step": int(host_logits[0].numel() * 4 + 4),
+           "steps": e2e_steps, "ms_per_step": w_s / e2e_steps * 1e3,
+           "how": "api.TrainSession, 2 untimed warm-up steps, then per step: pinned-host input "
+                  "rows H2D (prefetched one step ahead on a copy stream) + GCN row scaling, "
+                  "epoch, logits + loss D2H (overlapping the backward); host wall clock incl. "
+                  "final sync"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(g, ps, caps, budget_s=args.cpu_budget)
-    eng.close()
+    sess.close()
     if rank == 0:
         line = {
             "metric": "full-batch epoch GTEPS (L*|E|/epoch time)",

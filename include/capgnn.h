@@ -62,7 +62,7 @@ int cg_hash_labels(int32_t *out, const int32_t *vertex, int64_t n_rows, int C,
 /* X[r*ld + k] *= scale[r] (GCN source-degree pre-scaling of uploaded rows). */
 int cg_scale_rows(float *X, int64_t ld, int64_t n_rows, int F, const float *scale,
                   void *stream);
-/* dst[r*ldd + k] = src[r*lds + k] * scale[r]. */
+/* dst[r*ldd + k] = src[r*lds + k] * scale[r]  (scale NULL: plain row copy). */
 int cg_scale_rows_to(float *dst, int64_t ldd, const float *src, int64_t lds, int64_t n_rows,
                      int F, const float *scale, void *stream);
 
@@ -114,11 +114,13 @@ int cg_split_tf32(int64_t n, const float *x, float *hi, float *lo, void *stream)
  * K-major (one TMA box per k-block) weight operand.                      */
 int cg_split_tf32_t(int n_mats, const int64_t *off, const int32_t *rows, const int32_t *cols,
                     const float *x, float *hi, float *lo, int64_t max_elems, void *stream);
-/* dW[k, n] (+)= sum_m A[m, k] * D[m, n]; deterministic split over m.
+/* dW[k, n] = sum_m A[m, k] * D[m, n]; deterministic split over m.
+ * db (optional): db[n] = sum_m D[m, n] (the bias gradient) -- under 3xTF32
+ * fused into the same kernel (column sums while D is staged in smem).
  * ws must hold cg_wgrad_workspace(M, K, N) floats.                        */
 int64_t cg_wgrad_workspace(int64_t M, int K, int N);
 int cg_wgrad(int64_t M, int K, int N, const float *A, int64_t lda, const float *D,
-             int64_t ldd, float *dW, float *ws, int mode, void *stream);
+             int64_t ldd, float *dW, float *db, float *ws, int mode, void *stream);
 /* db[n] = sum_m D[m, n] (deterministic); ws as for cg_wgrad with K = 1.  */
 int cg_colsum(int64_t M, int N, const float *D, int64_t ldd, float *db, float *ws,
               void *stream);

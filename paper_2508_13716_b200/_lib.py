@@ -55,7 +55,7 @@ SIGNATURES = {
     "cg_split_tf32": [I64, P, P, P, P],
     "cg_split_tf32_t": [INT, P, P, P, P, P, P, I64, P],
     "cg_wgrad_workspace": [I64, INT, INT],
-    "cg_wgrad": [I64, INT, INT, P, I64, P, I64, P, P, INT, P],
+    "cg_wgrad": [I64, INT, INT, P, I64, P, I64, P, P, P, INT, P],
     "cg_colsum": [I64, INT, P, I64, P, P, P],
     "cg_softmax_ce": [I64, INT, P, I64, P, F32, P, I64, P, P, P],
     "cg_adam": [I64, P, P, P, P, F32, F32, F32, F32, INT, P, P, P],

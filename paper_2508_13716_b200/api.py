@@ -138,6 +138,170 @@ def _model_times(ps, sigma, nrm, cfg):
     return mix, comp
 
 
+class TrainSession:
+    """The drop-in's stepwise form: ``train()``'s setup once, then one real
+    training epoch per ``step()``.
+
+    Same leading arguments, validation and DomainErrors as halopart's
+    ``run()`` (simulator.py:160-184).  Per step the caller may hand in this
+    device's input rows from pinned host memory (``prefetch_features``: the
+    upload overlaps the previous epoch) and start non-blocking downloads of
+    the logits / loss (``fetch_logits`` / ``fetch_loss``); ``report()`` builds
+    the SimReport-compatible ``TrainReport`` of the steps taken so far.
+    """
+
+    def __init__(self, g, part, profiles, caps, cfg, record_trace: bool = False, *,
+                 model: str = "gcn", num_classes: int = 40, gemm: str = "fp32",
+                 plan_mode: str = "auto", keep_logits: str = "last", keep_params: bool = False,
+                 timers: bool = True, seed: int = 2):
+        import torch
+        from .comm import DistComm, SoloComm
+        from .engine import Engine
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("train() needs a CUDA device: the hot path has no CPU fallback")
+        ps, sigma = _resolve(part)
+        P = ps.P
+        nrm = _normalize(profiles)
+        if len(caps.c_gpu) != P:
+            raise DomainError(f"capacities cover {len(caps.c_gpu)} devices, partition has {P}")
+        if any(d >= len(nrm) for d in sigma):
+            raise DomainError("sigma names a device outside the profile list")
+        bpe = HG.feature_bytes(cfg.f_dim)
+        if bpe != caps.bytes_per_entry:
+            raise DomainError(
+                f"capacities sized for {caps.bytes_per_entry} B entries, config implies {bpe} B")
+        if model not in ("gcn", "sage"):
+            raise DomainError(f"unknown model {model!r}")
+        if any(int(f) % 4 for f in cfg.f_dim):
+            raise DomainError("layer widths must be multiples of 4 (pad the feature dim)")
+
+        dist_on = torch.distributed.is_available() and torch.distributed.is_initialized()
+        world = torch.distributed.get_world_size() if dist_on else 1
+        rank = torch.distributed.get_rank() if dist_on else 0
+        device = torch.cuda.current_device()
+        self.comm = DistComm(device) if world > 1 else SoloComm()
+
+        # importance ranking + warm (simulator.py:186-196), native and bit-exact
+        union, score = HG.influence_scores(g, ps)
+        ranked = [h[np.lexsort((h, -score[np.searchsorted(union, h)]))] for h in ps.halo]
+        self.planner = SequentialPlanner(cfg.policy, caps.c_cpu, caps.c_gpu, union, score,
+                                         [np.asarray(h, np.int64) for h in ps.halo], ranked)
+        self.planner.warm()
+        self.layout = build_layout(g, [np.asarray(x, np.int64) for x in ps.inner],
+                                   [np.asarray(h, np.int64) for h in ps.halo], caps.c_gpu,
+                                   world, model)
+        dims = [int(f) for f in cfg.f_dim] + [int(num_classes)]
+        from .models import init_params
+        params = init_params(model, dims, seed)
+        self.engine = Engine(self.layout, rank, model, dims, bpe, caps, self.planner,
+                             cfg.staleness_bound, cfg.policy, comm=self.comm, lr=0.01, gemm=gemm,
+                             params_init=params, device=device, record_outcomes=record_trace,
+                             plan_mode=plan_mode)
+        self.g, self.ps, self.cfg, self.sigma, self.bpe = g, ps, cfg, sigma, bpe
+        self.record_trace, self.keep_logits, self.keep_params = record_trace, keep_logits, keep_params
+        self.timers = timers
+        self.mix, self.comp = _model_times(ps, sigma, nrm, cfg)
+        self.world = world
+        self.epoch = 0
+        self.records, self.spans, self.rows = [], [], []
+        self.tot = np.zeros(3, np.int64)
+        self.rep = TrainReport(config=cfg.to_dict(), sigma=sigma, records=self.records,
+                               epoch_makespans=self.spans, total_time=0.0, total_fwd_bytes=0,
+                               total_bwd_bytes=0, hit_rate_local=0.0, hit_rate_global=0.0,
+                               n_edges=int(g.n_edges), n_layers=len(cfg.f_dim), n_devices=world)
+        if keep_logits == "all":
+            self.rep.logits_per_epoch = []
+        if keep_params:
+            self.rep.params_per_epoch = []   # weights at the START of each epoch
+        self._pending = []
+
+    # -- host I/O (all non-blocking; see Engine)
+    def prefetch_features(self, host_x) -> None:
+        """Upload this device's input rows for the NEXT step (pinned host)."""
+        self.engine.prefetch_features(host_x)
+
+    def fetch_logits(self, host_buf) -> None:
+        self.engine.fetch_logits(host_buf)
+
+    def fetch_loss(self, stats, host_buf) -> None:
+        self.engine.fetch_loss(stats, host_buf)
+
+    def step(self, sync: bool = True):
+        """Run one epoch.  With sync=False the epoch is only enqueued; its
+        record is completed by the next ``finish()``/``report()``."""
+        self.epoch += 1
+        e = self.epoch
+        if self.keep_params:
+            self.rep.params_per_epoch.append(self.engine.param_views())
+        stt = self.engine.run_epoch(e, timers=self.timers, sync=sync)
+        if sync:
+            self._record(stt)
+        else:
+            self._pending.append(stt)
+        return stt
+
+    def finish(self) -> None:
+        for stt in self._pending:
+            self._record(self.engine.finish(stt))
+        self._pending = []
+
+    def _record(self, stt) -> None:
+        rep, ps, cfg, e = self.rep, self.ps, self.cfg, stt.epoch
+        rep.losses.append(stt.loss)
+        rep.epoch_seconds.append(stt.seconds)
+        rep.spmm_fwd_ms.append(stt.spmm_fwd_ms)
+        rep.spmm_bwd_ms.append(stt.spmm_bwd_ms)
+        rep.planner.append(stt.planner)
+        if self.keep_logits == "all":
+            rep.logits_per_epoch.append(_gather_logits(self.engine, self.comm,
+                                                       self.g.n_vertices))
+        dts = []
+        for i in range(ps.P):
+            lh, gh, ms = (int(x) for x in stt.counts[i])
+            self.tot += (lh, gh, ms)
+            c = (ms + ps.cut_edges[i]) * self.mix[i] * cfg.unit_time
+            ov = min(1.0, cfg.prefetch_depth / max(1, len(ps.halo[i])))
+            resid = c - min(c, self.comp[i]) * ov
+            dt = self.comp[i] + resid
+            dts.append(dt)
+            self.records.append(EpochDeviceRecord(
+                epoch=e, device=i, fwd_bytes=ms * self.bpe, bwd_bytes=ps.cut_edges[i] * self.bpe,
+                local_hits=lh, global_hits=gh, misses=ms, compute_time=self.comp[i],
+                comm_time=c, residual_comm_time=resid, device_time=dt))
+        self.spans.append(max(dts))
+        if self.record_trace:
+            oc = self.engine.gpu_outcomes() if stt.planner == "gpu" else None
+            self.rows += _trace_rows(self.planner, e, oc)
+
+    def report(self) -> TrainReport:
+        self.finish()
+        rep = self.rep
+        if self.keep_logits in ("last", "all"):
+            rep.logits = (rep.logits_per_epoch[-1] if self.keep_logits == "all"
+                          and rep.logits_per_epoch else
+                          _gather_logits(self.engine, self.comm, self.g.n_vertices))
+        rep.params = self.engine.param_views()
+        rep.total_time = sum(self.spans)
+        rep.total_fwd_bytes = sum(r.fwd_bytes for r in self.records)
+        rep.total_bwd_bytes = sum(r.bwd_bytes for r in self.records)
+        look = int(self.tot.sum())
+        rep.hit_rate_local = int(self.tot[0]) / look if look else 0.0
+        rep.hit_rate_global = int(self.tot[1]) / look if look else 0.0
+        if self.record_trace:
+            rep.trace_csv = trace_csv(self.rows)
+        return rep
+
+    def close(self) -> None:
+        self.engine.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
 def train(g, part, profiles, caps, cfg, record_trace: bool = False, *, model: str = "gcn",
           num_classes: int = 40, gemm: str = "fp32", plan_mode: str = "auto",
           keep_logits: str = "last", keep_params: bool = False, timers: bool = True,
@@ -148,106 +312,15 @@ def train(g, part, profiles, caps, cfg, record_trace: bool = False, *, model: st
     world size P (or P/world slots per GPU); otherwise every partition runs
     on the current GPU, each with its own local cache level.
     """
-    import torch
-    from .comm import DistComm, SoloComm
-    from .engine import Engine
-
-    if not torch.cuda.is_available():
-        raise RuntimeError("train() needs a CUDA device: the hot path has no CPU fallback")
-    ps, sigma = _resolve(part)
-    P = ps.P
-    nrm = _normalize(profiles)
-    if len(caps.c_gpu) != P:
-        raise DomainError(f"capacities cover {len(caps.c_gpu)} devices, partition has {P}")
-    if any(d >= len(nrm) for d in sigma):
-        raise DomainError("sigma names a device outside the profile list")
-    bpe = HG.feature_bytes(cfg.f_dim)
-    if bpe != caps.bytes_per_entry:
-        raise DomainError(
-            f"capacities sized for {caps.bytes_per_entry} B entries, config implies {bpe} B")
-    if model not in ("gcn", "sage"):
-        raise DomainError(f"unknown model {model!r}")
-    if any(int(f) % 4 for f in cfg.f_dim):
-        raise DomainError("layer widths must be multiples of 4 (pad the feature dim)")
-
-    dist_on = torch.distributed.is_available() and torch.distributed.is_initialized()
-    world = torch.distributed.get_world_size() if dist_on else 1
-    rank = torch.distributed.get_rank() if dist_on else 0
-    device = torch.cuda.current_device()
-    comm = DistComm(device) if world > 1 else SoloComm()
-
-    # importance ranking + warm (simulator.py:186-196), native and bit-exact
-    union, score = HG.influence_scores(g, ps)
-    ranked = [h[np.lexsort((h, -score[np.searchsorted(union, h)]))] for h in ps.halo]
-    planner = SequentialPlanner(cfg.policy, caps.c_cpu, caps.c_gpu, union, score,
-                                [np.asarray(h, np.int64) for h in ps.halo], ranked)
-    planner.warm()
-    layout = build_layout(g, [np.asarray(x, np.int64) for x in ps.inner],
-                          [np.asarray(h, np.int64) for h in ps.halo], caps.c_gpu, world, model)
-    dims = [int(f) for f in cfg.f_dim] + [int(num_classes)]
-    from .models import init_params
-    params = init_params(model, dims, seed)
-    eng = Engine(layout, rank, model, dims, bpe, caps, planner, cfg.staleness_bound,
-                 cfg.policy, comm=comm, lr=0.01, gemm=gemm, params_init=params,
-                 device=device, record_outcomes=record_trace, plan_mode=plan_mode)
-
-    mix, comp = _model_times(ps, sigma, nrm, cfg)
-    records, spans, rows = [], [], []
-    rep = TrainReport(config=cfg.to_dict(), sigma=sigma, records=records, epoch_makespans=spans,
-                      total_time=0.0, total_fwd_bytes=0, total_bwd_bytes=0,
-                      hit_rate_local=0.0, hit_rate_global=0.0, n_edges=int(g.n_edges),
-                      n_layers=len(cfg.f_dim), n_devices=world)
-    if keep_logits == "all":
-        rep.logits_per_epoch = []
-    if keep_params:
-        rep.params_per_epoch = []   # weights at the START of each epoch
-    tot = np.zeros(3, np.int64)
-    try:
-        for e in range(1, cfg.epochs + 1):
-            if keep_params:
-                rep.params_per_epoch.append(eng.param_views())
-            stt = eng.run_epoch(e, timers=timers)
-            rep.losses.append(stt.loss)
-            rep.epoch_seconds.append(stt.seconds)
-            rep.spmm_fwd_ms.append(stt.spmm_fwd_ms)
-            rep.spmm_bwd_ms.append(stt.spmm_bwd_ms)
-            rep.planner.append(stt.planner)
-            if keep_logits == "all":
-                rep.logits_per_epoch.append(_gather_logits(eng, comm, g.n_vertices))
-            dts = []
-            for i in range(P):
-                lh, gh, ms = (int(x) for x in stt.counts[i])
-                tot += (lh, gh, ms)
-                c = (ms + ps.cut_edges[i]) * mix[i] * cfg.unit_time
-                ov = min(1.0, cfg.prefetch_depth / max(1, len(ps.halo[i])))
-                resid = c - min(c, comp[i]) * ov
-                dt = comp[i] + resid
-                dts.append(dt)
-                records.append(EpochDeviceRecord(
-                    epoch=e, device=i, fwd_bytes=ms * bpe, bwd_bytes=ps.cut_edges[i] * bpe,
-                    local_hits=lh, global_hits=gh, misses=ms, compute_time=comp[i],
-                    comm_time=c, residual_comm_time=resid, device_time=dt))
-            spans.append(max(dts))
-            if record_trace:
-                oc = eng.gpu_outcomes() if stt.planner == "gpu" else None
-                rows += _trace_rows(planner, e, oc)
+    with TrainSession(g, part, profiles, caps, cfg, record_trace, model=model,
+                      num_classes=num_classes, gemm=gemm, plan_mode=plan_mode,
+                      keep_logits=keep_logits, keep_params=keep_params, timers=timers,
+                      seed=seed) as sess:
+        for _ in range(cfg.epochs):
+            stt = sess.step()
             if on_epoch is not None:
-                on_epoch(e, stt, eng)
-        if keep_logits in ("last", "all"):
-            rep.logits = (rep.logits_per_epoch[-1] if keep_logits == "all"
-                          else _gather_logits(eng, comm, g.n_vertices))
-        rep.params = eng.param_views()
-    finally:
-        eng.close()
-    rep.total_time = sum(spans)
-    rep.total_fwd_bytes = sum(r.fwd_bytes for r in records)
-    rep.total_bwd_bytes = sum(r.bwd_bytes for r in records)
-    look = int(tot.sum())
-    rep.hit_rate_local = int(tot[0]) / look if look else 0.0
-    rep.hit_rate_global = int(tot[1]) / look if look else 0.0
-    if record_trace:
-        rep.trace_csv = trace_csv(rows)
-    return rep
+                on_epoch(stt.epoch, stt, sess.engine)
+        return sess.report()
 
 
 def _trace_rows(planner: SequentialPlanner, e: int, outcomes):

@@ -22,7 +22,10 @@ int cg_gemm_tc(int64_t M, int N, int K1, const float *A1, int64_t lda1, const fl
                int relu, const float *row_scale, const float *mask, int64_t ldm, float *C,
                int64_t ldc, int mode, const float *B1_lo, const float *B2_lo, cudaStream_t st);
 int cg_wgrad_tc(int64_t M, int K, int N, const float *A, int64_t lda, const float *D, int64_t ldd,
-                float *ws, int64_t chunk, int64_t n_chunks, int mode, cudaStream_t st);
+                float *ws, int64_t chunk, int64_t n_chunks, int mode, float *bws,
+                cudaStream_t st);
+int cg_colsum(int64_t M, int N, const float *D, int64_t ldd, float *db, float *ws, void *stream);
+int cg_reduce_chunks(int64_t n_out, int64_t n_chunks, const float *ws, float *out, cudaStream_t st);
 
 namespace {
 
@@ -159,22 +162,6 @@ k_wgrad_partial(int64_t M, int K, int N, const float *__restrict__ A, int64_t ld
     }
 }
 
-__global__ void k_wgrad_reduce(int64_t n_out, int64_t n_chunks, const float *__restrict__ ws,
-                               float *__restrict__ out) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n_out) return;
-    // four independent chains (pipelined loads), combined in a fixed order
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-    int64_t c = 0;
-    for (; c + 3 < n_chunks; c += 4) {
-        s0 += ws[c * n_out + i];
-        s1 += ws[(c + 1) * n_out + i];
-        s2 += ws[(c + 2) * n_out + i];
-        s3 += ws[(c + 3) * n_out + i];
-    }
-    for (; c < n_chunks; ++c) s0 += ws[c * n_out + i];
-    out[i] = (s0 + s1) + (s2 + s3);
-}
 
 constexpr int64_t kWgradChunk = 1024;  // minimum split-K chunk (SIMT path: always this)
 
@@ -212,19 +199,28 @@ int cg_gemm(int64_t M, int N, int K1, const float *A1, int64_t lda1, const float
 int64_t cg_wgrad_workspace(int64_t M, int K, int N) {
     int64_t nch = (M + kWgradChunk - 1) / kWgradChunk;
     if (nch < 1) nch = 1;
-    return nch * (int64_t)K * N;
+    // dW partials + bias partials (4 per chunk) or the column-sum fallback's
+    const int64_t col = ((M + 255) / 256) * N;
+    const int64_t bias = nch * 4 * (int64_t)N;
+    return nch * (int64_t)K * N + (col > bias ? col : bias) + 4;
 }
 
 int cg_wgrad(int64_t M, int K, int N, const float *A, int64_t lda, const float *D, int64_t ldd,
-             float *dW, float *ws, int mode, void *stream) {
+             float *dW, float *db, float *ws, int mode, void *stream) {
     if (K == 0 || N == 0) return 0;
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t chunk = (mode == 1 || mode == 2) ? wgrad_chunk_tc(M, K, N) : kWgradChunk;
     int64_t nch = (M + chunk - 1) / chunk;
     if (nch < 1) nch = 1;
     int launched = 0;
+    // bias gradient: fused into the 3xTF32 kernel (column sums of D while it
+    // is split in shared memory), else the standalone column sum
+    float *bws = ws + nch * (int64_t)K * N;
+    bws = reinterpret_cast<float *>(((uintptr_t)bws + 15) & ~(uintptr_t)15);
+    const bool fuse_db = db && mode == 1 && !(N % 4);
     if (mode == 1 || mode == 2) {
-        int rc = cg_wgrad_tc(M, K, N, A, lda, D, ldd, ws, chunk, nch, mode, st);
+        int rc = cg_wgrad_tc(M, K, N, A, lda, D, ldd, ws, chunk, nch, mode,
+                             fuse_db ? bws : nullptr, st);
         if (rc < 0) return rc;
         launched += rc;
     } else {
@@ -233,9 +229,20 @@ int cg_wgrad(int64_t M, int K, int N, const float *A, int64_t lda, const float *
         launched += 1;
     }
     int64_t n_out = (int64_t)K * N;
-    k_wgrad_reduce<<<(unsigned)((n_out + 255) / 256), 256, 0, st>>>(n_out, nch, ws, dW);
+    int rc = cg_reduce_chunks(n_out, nch, ws, dW, st);   // 8 warps split the chunks
+    if (rc < 0) return rc;
+    launched += rc;
+    if (fuse_db) {
+        rc = cg_reduce_chunks(N, nch * 4, bws, db, st);
+        if (rc < 0) return rc;
+        launched += rc;
+    } else if (db) {
+        int rc = cg_colsum(M, N, D, ldd, db, bws, stream);
+        if (rc < 0) return rc;
+        launched += rc;
+    }
     cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? launched + 1 : cg_cuda_fail(e, "cg_wgrad");
+    return e == cudaSuccess ? launched : cg_cuda_fail(e, "cg_wgrad");
 }
 
 }  // extern "C"

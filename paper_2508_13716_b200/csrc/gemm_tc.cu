@@ -76,6 +76,8 @@ struct Params {
     int b_lo_off;    // offset of B_lo from the B slice in a stage
     int acc_stride;  // TMEM columns between the two accumulator buffers
     int tma_store;   // C written by TMA bulk tensor stores (mC is valid)
+    float *bws;      // weight gradient only: per (chunk, splitter warp) column sums
+                     // of the MN-major B operand (= the bias gradient partials)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -108,6 +110,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
             : "r"(a), "r"(parity)
             : "memory");
     } while (!done);
+}
+
+__device__ __forceinline__ uint32_t rn_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r;
+}
+
+// x - trunc_tf32(x), rounded to a TF32 value (|error| <= 2^-12 |x - trunc|)
+__device__ __forceinline__ uint32_t lo_of_trunc(uint32_t x) {
+    return rn_tf32(__uint_as_float(x) - __uint_as_float(x & 0xFFFFE000u));
 }
 
 __device__ __forceinline__ bool elect_one() {
@@ -408,9 +421,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                     if (p.a_tmem) {
                         // A (= its TF32 truncation) and A_lo sit in TMEM slot s
                         mma_kblock_ts3(tmem_d, tmem_base + A_TMEM_COL + 64 * s,
-                                       smem_desc(sb, b_lbo, b_sbo, b_lay),
-                                       smem_desc(sb_lo, b_lbo, b_sbo, b_lay), b_step >> 4, idesc,
-                                       first ? 0u : 1u, &empty[s]);
+                                           smem_desc(sb, b_lbo, b_sbo, b_lay),
+                                           smem_desc(sb_lo, b_lbo, b_sbo, b_lay), b_step >> 4,
+                                           idesc, first ? 0u : 1u, &empty[s]);
                         first = false;
                         __syncwarp();
                         continue;
@@ -575,6 +588,11 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
         uint32_t it = 0;
         for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
             const TileCoord tc = tile_of(p, t, n_tiles, m_tiles);
+            // bias-gradient partials: only the first row tile of each (n, chunk)
+            const bool bws_on = p.bws != nullptr && tc.m0 == 0;
+            float4 bacc[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) bacc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
             for (int o = 0; o < p.n_ops; ++o) {
                 int kb0, nkb;
                 kblocks(p, o, tc.z, kb0, nkb);
@@ -612,21 +630,34 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                             const uint4 *bh = reinterpret_cast<const uint4 *>(smem + s * stage_bytes + A_BYTES);
                             uint4 *bl = reinterpret_cast<uint4 *>(smem + s * stage_bytes + A_BYTES + p.b_lo_off);
                             const int t128 = threadIdx.x - 256;
-#pragma unroll 4
-                            for (int i = t128; i < nb16; i += 128) {
+                            const bool bsum = bws_on && p.op[o].b_mn;
+#pragma unroll 8
+                            for (int k = 0; k < 8; ++k) {
+                                const int i = t128 + 128 * k;
+                                if (i >= nb16) break;
                                 const uint4 w = bh[i];
-                                bl[i] = make_uint4(
-                                    __float_as_uint(__uint_as_float(w.x) - __uint_as_float(w.x & 0xFFFFE000u)),
-                                    __float_as_uint(__uint_as_float(w.y) - __uint_as_float(w.y & 0xFFFFE000u)),
-                                    __float_as_uint(__uint_as_float(w.z) - __uint_as_float(w.z & 0xFFFFE000u)),
-                                    __float_as_uint(__uint_as_float(w.w) - __uint_as_float(w.w & 0xFFFFE000u)));
+                                // B stays raw in smem (the MMA truncates it to
+                                // TF32); B_lo = TF32(B - trunc(B))
+                                bl[i] = make_uint4(lo_of_trunc(w.x), lo_of_trunc(w.y),
+                                                   lo_of_trunc(w.z), lo_of_trunc(w.w));
+                                if (bsum) {
+                                    // MN-major box k/2, this thread's column quad is
+                                    // fixed (see the combine below); rows vary with k
+                                    float4 &a4 = bacc[k >> 1];
+                                    a4.x += __uint_as_float(w.x); a4.y += __uint_as_float(w.y);
+                                    a4.z += __uint_as_float(w.z); a4.w += __uint_as_float(w.w);
+                                }
                             }
                             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                         }
 #pragma unroll
-                        for (int i = 0; i < 32; ++i)
-                            lv[i] = __float_as_uint(__uint_as_float(hv[i]) -
-                                                    __uint_as_float(hv[i] & 0xFFFFE000u));
+                        for (int i = 0; i < 32; ++i) {
+                            // hi = RN TF32(x), lo = RN TF32(x - hi): both exact
+                            // TF32 values, |x - hi - lo| <= 2^-23 |x|
+                            const float x = __uint_as_float(hv[i]);
+                            hv[i] = rn_tf32(x);
+                            lv[i] = rn_tf32(x - __uint_as_float(hv[i]));
+                        }
                         const uint32_t ta = tmem_base + ((uint32_t)(32 * q) << 16) + A_TMEM_COL + 64 * s;
                         tmem_st32(ta, hv);
                         tmem_st32(ta + 32, lv);
@@ -658,6 +689,39 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                     }
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     mbar_arrive(&conv[s]);
+                }
+            }
+            if (bws_on) {
+                // Thread t of the splitter warp group owns column quad
+                // 8*(((t&7)>>1) ^ ((t>>3)&3)) + 4*(t&1) of every 32-column box
+                // (128B-swizzle, 32B atoms: atom c of row v at c ^ (v & 3)).  The
+                // 4 lanes of a warp sharing a quad are lane ^ 10 and lane ^ 20:
+                // butterfly them, lanes 0..7 hold the warp's 8-row sums.
+                const int lw = lane;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    float4 &a4 = bacc[k];
+#pragma unroll
+                    for (int sh = 10; sh <= 20; sh += 10) {
+                        a4.x += __shfl_xor_sync(0xffffffffu, a4.x, sh);
+                        a4.y += __shfl_xor_sync(0xffffffffu, a4.y, sh);
+                        a4.z += __shfl_xor_sync(0xffffffffu, a4.z, sh);
+                        a4.w += __shfl_xor_sync(0xffffffffu, a4.w, sh);
+                    }
+                }
+                if (lw < 8) {
+                    const int cq = 8 * (lw >> 1) + 4 * (lw & 1);
+                    float *dst = p.bws + ((int64_t)tc.z * 4 + (warp & 3)) * p.N;
+                    for (int k = 0; k < nb_b && k < 4; ++k) {
+                        const int n = tc.n0 + 32 * k + cq;
+                        if (n + 3 < p.N) {
+                            *reinterpret_cast<float4 *>(dst + n) = bacc[k];
+                        } else {
+                            if (n < p.N) dst[n] = bacc[k].x;
+                            if (n + 1 < p.N) dst[n + 1] = bacc[k].y;
+                            if (n + 2 < p.N) dst[n + 2] = bacc[k].z;
+                        }
+                    }
                 }
             }
         }
@@ -857,7 +921,8 @@ int cg_gemm_tc(int64_t M, int N, int K1, const float *A1, int64_t lda1, const fl
 
 // Partial weight gradients: ws[c][k][n] = sum_{m in chunk c} A[m, k] D[m, n].
 int cg_wgrad_tc(int64_t M, int K, int N, const float *A, int64_t lda, const float *D, int64_t ldd,
-                float *ws, int64_t chunk, int64_t n_chunks, int mode, cudaStream_t st) {
+                float *ws, int64_t chunk, int64_t n_chunks, int mode, float *bws,
+                cudaStream_t st) {
     using namespace tc;
     if ((lda % 4) || (ldd % 4) || ((uintptr_t)A % 16) || ((uintptr_t)D % 16)) {
         cg_set_error("cg_wgrad_tc: operands must be 16-byte aligned with ld % 4 == 0");
@@ -876,6 +941,7 @@ int cg_wgrad_tc(int64_t M, int K, int N, const float *A, int64_t lda, const floa
     p.C = ws;
     p.ldc = N;
     p.vec_ok = !(N % 4) && !((uintptr_t)ws % 16);
+    p.bws = bws;   // caller passes it only for the 3xTF32 path (MN-major B, TMEM A)
     CUtensorMap ma, mb;
     if (!make_map(&ma, A, K, M, lda, BK, true) || !make_map(&mb, D, N, M, ldd, BK, true)) {
         cg_set_error("cg_wgrad_tc: cuTensorMapEncodeTiled failed");

@@ -270,6 +270,87 @@ k_softmax_ce(int64_t n, int C, const float *__restrict__ logits, int64_t ld,
     }
 }
 
+// Narrow-class variant (C <= 64, ld % 4 == 0, ldg % 4 == 0, 16-B aligned rows):
+// 4 lanes per row, each holding up to 4 float4 of logits in registers, so a
+// row costs one 16-byte load / store per 4 classes and two shuffle rounds.
+template <int NV>
+__global__ void __launch_bounds__(256)
+k_softmax_ce4(int64_t n, int C, const float *__restrict__ logits, int64_t ld,
+              const int32_t *__restrict__ label, float inv_n, float *__restrict__ grad,
+              int64_t ldg, float *__restrict__ block_loss) {
+    __shared__ float wl[8];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int sub = lane & 3;                       // lane within the row group
+    const int C4 = (C + 3) >> 2;
+    float acc = 0.f;
+    // the loop bound is warp-uniform (shuffles below need every lane)
+    const int64_t stride = (int64_t)gridDim.x * 64;
+    for (int64_t r0 = ((int64_t)blockIdx.x * 256 + (threadIdx.x & ~31)) >> 2; r0 < n;
+         r0 += stride) {
+        const int64_t r = r0 + (lane >> 2);
+        const bool ok = r < n;
+        const float4 *z4 = reinterpret_cast<const float4 *>(logits + (ok ? r : 0) * ld);
+        float4 v[NV];
+        float mx = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int c4 = sub + 4 * k;
+            if (ok && c4 < C4) {
+                v[k] = __ldg(z4 + c4);
+                const int c = 4 * c4;
+                if (c + 0 >= C) v[k].x = -INFINITY;
+                if (c + 1 >= C) v[k].y = -INFINITY;
+                if (c + 2 >= C) v[k].z = -INFINITY;
+                if (c + 3 >= C) v[k].w = -INFINITY;
+            } else {
+                v[k] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+            }
+            mx = fmaxf(mx, fmaxf(fmaxf(v[k].x, v[k].y), fmaxf(v[k].z, v[k].w)));
+        }
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        float se = 0.f;
+#pragma unroll
+        for (int k = 0; k < NV; ++k)
+            se += __expf(v[k].x - mx) + __expf(v[k].y - mx) + __expf(v[k].z - mx) +
+                  __expf(v[k].w - mx);
+        se += __shfl_xor_sync(0xffffffffu, se, 1);
+        se += __shfl_xor_sync(0xffffffffu, se, 2);
+        const float lse = __logf(se);
+        const int y = ok ? label[r] : -1;
+        float zy = 0.f;
+        float4 *g4 = reinterpret_cast<float4 *>(grad + (ok ? r : 0) * ldg);
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int c4 = sub + 4 * k;
+            if (!ok || c4 >= C4) continue;
+            const int c = 4 * c4;
+            float4 p;
+            p.x = c + 0 < C ? (__expf(v[k].x - mx - lse) - (c + 0 == y ? 1.f : 0.f)) * inv_n : 0.f;
+            p.y = c + 1 < C ? (__expf(v[k].y - mx - lse) - (c + 1 == y ? 1.f : 0.f)) * inv_n : 0.f;
+            p.z = c + 2 < C ? (__expf(v[k].z - mx - lse) - (c + 2 == y ? 1.f : 0.f)) * inv_n : 0.f;
+            p.w = c + 3 < C ? (__expf(v[k].w - mx - lse) - (c + 3 == y ? 1.f : 0.f)) * inv_n : 0.f;
+            if (y >= c && y < c + 4) zy = (y == c) ? v[k].x : (y == c + 1) ? v[k].y
+                                        : (y == c + 2) ? v[k].z : v[k].w;
+            g4[c4] = p;
+        }
+        zy += __shfl_xor_sync(0xffffffffu, zy, 1);
+        zy += __shfl_xor_sync(0xffffffffu, zy, 2);
+        if (ok && sub == 0) acc += lse - (zy - mx);
+    }
+    // fixed-order combine: lanes of a warp by butterfly, warps in order
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) wl[w] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) t += wl[k];
+        block_loss[blockIdx.x] = t;
+    }
+}
+
 // Deterministic sum of x[0..n) into *out (single block, fixed order).
 __global__ void k_sum_fixed(const float *__restrict__ x, int64_t n, float *__restrict__ out) {
     __shared__ double sh[1024];
@@ -367,13 +448,37 @@ __global__ void k_scale_rows_to(float *__restrict__ dst, int64_t ldd, const floa
          i += (int64_t)gridDim.x * blockDim.x) {
         int64_t r = i / F;
         int64_t c = i - r * F;
-        dst[r * ldd + c] = src[r * lds + c] * scale[r];
+        dst[r * ldd + c] = src[r * lds + c] * (scale ? scale[r] : 1.f);
     }
 }
 
+// float4 variant (F, ldd, lds multiples of 4, 16-byte aligned rows)
+__global__ void k_scale_rows_to4(float *__restrict__ dst, int64_t ldd, const float *__restrict__ src,
+                                 int64_t lds, int64_t n, int F4, const float *__restrict__ scale) {
+    const int64_t total = n * (int64_t)F4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / F4;
+        const int64_t c = i - r * F4;
+        float4 v = __ldg(reinterpret_cast<const float4 *>(src + r * lds) + c);
+        const float sc = scale ? __ldg(scale + r) : 1.f;
+        v.x *= sc; v.y *= sc; v.z *= sc; v.w *= sc;
+        reinterpret_cast<float4 *>(dst + r * ldd)[c] = v;
+    }
+}
+
+__device__ __forceinline__ uint32_t rn_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r;
+}
+
+// x ~= hi + lo with hi = round-to-nearest TF32(x) and lo = TF32(x - hi), both
+// exact TF32 values (the tensor core's operand truncation is then lossless):
+// |x - hi - lo| <= 2^-23 |x|.
 __device__ __forceinline__ void split_tf32(float x, float &hi, float &lo) {
-    hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-    lo = x - hi;
+    hi = __uint_as_float(rn_tf32(x));
+    lo = __uint_as_float(rn_tf32(x - hi));
 }
 
 __global__ void k_adam(int64_t n, float *__restrict__ p, const float *__restrict__ g,
@@ -548,6 +653,16 @@ inline int grid_for(int64_t work, int threads, int max_blocks = 148 * 16) {
 
 }  // namespace
 
+// out[i] = sum_c ws[c][i] over n_chunks partial rows, fixed order (internal
+// helper shared with the weight-gradient path in gemm.cu; not in the ABI).
+int cg_reduce_chunks(int64_t n_out, int64_t n_chunks, const float *ws, float *out,
+                     cudaStream_t st) {
+    if (n_out == 0) return 0;
+    k_reduce_chunks_tree<<<(unsigned)((n_out + 31) / 32), 256, 0, st>>>(n_out, n_chunks, ws, out);
+    CG_CHECK_LAUNCH("k_reduce_chunks_tree");
+    return 1;
+}
+
 extern "C" {
 
 int cg_hash_features(float *out, int64_t ld, const int32_t *vertex, int64_t n_rows, int F,
@@ -639,6 +754,12 @@ int cg_scale_rows(float *X, int64_t ld, int64_t n_rows, int F, const float *scal
 int cg_scale_rows_to(float *dst, int64_t ldd, const float *src, int64_t lds, int64_t n_rows,
                      int F, const float *scale, void *stream) {
     if (n_rows == 0 || F == 0) return 0;
+    if (!(F % 4) && !(ldd % 4) && !(lds % 4) && !((uintptr_t)dst % 16) && !((uintptr_t)src % 16)) {
+        k_scale_rows_to4<<<grid_for(n_rows * (F / 4), 256, n_sms() * 8), 256, 0,
+                           (cudaStream_t)stream>>>(dst, ldd, src, lds, n_rows, F / 4, scale);
+        CG_CHECK_LAUNCH("k_scale_rows_to4");
+        return 1;
+    }
     k_scale_rows_to<<<grid_for(n_rows * F, 256), 256, 0, (cudaStream_t)stream>>>(
         dst, ldd, src, lds, n_rows, F, scale);
     CG_CHECK_LAUNCH("k_scale_rows_to");
@@ -661,8 +782,21 @@ int cg_softmax_ce(int64_t n_rows, int C, const float *logits, int64_t ld, const 
                   void *stream) {
     if (n_rows == 0) return 0;
     cudaStream_t st = (cudaStream_t)stream;
-    const int blocks = grid_for(n_rows * 32, 256, 148 * 8);
-    k_softmax_ce<<<blocks, 256, 0, st>>>(n_rows, C, logits, ld, label, inv_n, grad, ldg, ws);
+    const bool narrow = C <= 64 && !(ld % 4) && !(ldg % 4) && !((uintptr_t)logits % 16) &&
+                        !((uintptr_t)grad % 16);
+    int blocks;
+    if (narrow) {
+        blocks = grid_for(n_rows * 4, 256, n_sms() * 8);
+        if (C <= 32)
+            k_softmax_ce4<2><<<blocks, 256, 0, st>>>(n_rows, C, logits, ld, label, inv_n, grad,
+                                                     ldg, ws);
+        else
+            k_softmax_ce4<4><<<blocks, 256, 0, st>>>(n_rows, C, logits, ld, label, inv_n, grad,
+                                                     ldg, ws);
+    } else {
+        blocks = grid_for(n_rows * 32, 256, 148 * 8);
+        k_softmax_ce<<<blocks, 256, 0, st>>>(n_rows, C, logits, ld, label, inv_n, grad, ldg, ws);
+    }
     k_sum_fixed<<<1, 1024, 0, st>>>(ws, blocks, loss_out);
     CG_CHECK_LAUNCH("cg_softmax_ce");
     return 2;

@@ -9,6 +9,7 @@ events and torch.distributed.  See DESIGN.md §4-§6.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -62,6 +63,8 @@ class Engine:
         self.policy = policy
         self.lr = lr
         self.gemm_mode = GEMM_MODES[gemm]
+        # experiment knob (diagnostics only): weight-gradient GEMM mode override
+        self.wgrad_mode = GEMM_MODES[os.environ.get("CG_WGRAD_MODE", gemm)]
         self.dev = torch.device("cuda", device if device is not None else torch.cuda.current_device())
         self.record_outcomes = record_outcomes
         self.plan_mode = plan_mode
@@ -195,6 +198,7 @@ class Engine:
         self.T = torch.zeros(D.n_in, max(self.dims[1:]), dtype=f32, device=dev)
         # frozen-plan (K6) state, created at hand-off
         self.k6 = None
+        self._io = None
         self.loss_dev = torch.zeros(1, dtype=f32, device=dev)
         torch.cuda.current_stream(self.dev).synchronize()
 
@@ -418,6 +422,7 @@ class Engine:
         if timers:
             t0.record()
         mode, hcounts, _ = self.plan(e)
+        self._consume_input()
         fwd_ev, bwd_ev = [], []
         n_in = D.n_in
         # ---------------- forward
@@ -443,6 +448,10 @@ class Engine:
                 self._copy(n, F, sid, srow, dst, self.tab[l], self.tab_ld[l], self.X[l], F)
             last = l == nL - 1
             out = self.logits if last else self.X[l + 1]
+            if last and self._io is not None and self._io["logits_done"] is not None:
+                # the previous epoch's logits download must finish first
+                torch.cuda.current_stream(self.dev).wait_event(self._io["logits_done"])
+                self._io["logits_done"] = None
             if kind == "gcn":
                 self._gemm(n_in, Fo, F, ptr(self.Z[l]), F, 2 * l, trans_b=0,
                            bias=self._p(2 * l + 1), relu=0 if last else 1,
@@ -451,6 +460,10 @@ class Engine:
                 self._gemm(n_in, Fo, F, ptr(self.X[l]), F, 3 * l, F, ptr(self.Z[l]), F,
                            3 * l + 1, trans_b=0, bias=self._p(3 * l + 2),
                            relu=0 if last else 1, C=ptr(out), ldc=Fo)
+        if self._io is not None:
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(self.dev))
+            self._io["fwd"] = ev
         # ---------------- loss
         n_total = self.L.n
         loss_ptr = ptr(self.grads) + 4 * self.n_params
@@ -461,16 +474,16 @@ class Engine:
         for l in range(nL - 1, -1, -1):
             F, Fo = self.F[l], self.dims[l + 1]
             dY = self.dL if l == nL - 1 else self.dY[cur]
+            # weight gradient(s); the bias gradient (column sums of dY) rides
+            # along in the same launch
             if kind == "gcn":
                 call("cg_wgrad", n_in, F, Fo, ptr(self.Z[l]), F, ptr(dY), Fo, self._g(2 * l),
-                     ptr(self.ws), self.gemm_mode, st)
-                call("cg_colsum", n_in, Fo, ptr(dY), Fo, self._g(2 * l + 1), ptr(self.ws), st)
+                     self._g(2 * l + 1), ptr(self.ws), self.wgrad_mode, st)
             else:
                 call("cg_wgrad", n_in, F, Fo, ptr(self.X[l]), F, ptr(dY), Fo, self._g(3 * l),
-                     ptr(self.ws), self.gemm_mode, st)
+                     None, ptr(self.ws), self.wgrad_mode, st)
                 call("cg_wgrad", n_in, F, Fo, ptr(self.Z[l]), F, ptr(dY), Fo,
-                     self._g(3 * l + 1), ptr(self.ws), self.gemm_mode, st)
-                call("cg_colsum", n_in, Fo, ptr(dY), Fo, self._g(3 * l + 2), ptr(self.ws), st)
+                     self._g(3 * l + 1), self._g(3 * l + 2), ptr(self.ws), self.wgrad_mode, st)
             if l == 0:
                 break
             nxt = self.dY[1 - cur] if l != nL - 1 else self.dY[cur]
@@ -561,6 +574,70 @@ class Engine:
             stats.spmm_bwd_ms = [a.elapsed_time(b) for a, b in stats.spmm_bwd_ms]
             stats.events = None
         return stats
+
+    # ------------------------------------------------------------ host I/O
+    # An input/output pipeline on two copy streams, so the per-step host
+    # traffic overlaps the epoch: the NEXT step's input rows are uploaded
+    # (H2D) while this step trains, and this step's logits are downloaded
+    # (D2H) during its backward pass.  Ordering is by CUDA events only.
+    def _io_state(self):
+        if self._io is None:
+            self._io = dict(h2d=torch.cuda.Stream(self.dev), d2h=torch.cuda.Stream(self.dev),
+                            stage=torch.empty(self.D.n_in, self.F[0], dtype=torch.float32,
+                                              device=self.dev),
+                            ready=None, free=None, logits_done=None, fwd=None)
+        return self._io
+
+    def prefetch_features(self, host_x) -> None:
+        """Start the H2D copy of the next epoch's input rows (pinned host,
+        raw features, this device's inner rows) on the upload stream; the
+        next run_epoch waits for it and scales the rows into X_0."""
+        io = self._io_state()
+        st = io["h2d"]
+        if io["free"] is not None:
+            st.wait_event(io["free"])      # the previous upload has been consumed
+        with torch.cuda.stream(st):
+            io["stage"].copy_(host_x, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(st)
+        io["ready"] = ev
+
+    def _consume_input(self) -> None:
+        io = self._io
+        if io is None or io["ready"] is None:
+            return
+        cs = torch.cuda.current_stream(self.dev)
+        cs.wait_event(io["ready"])
+        F0 = self.F[0]
+        call("cg_scale_rows_to", ptr(self.X[0]), F0, ptr(io["stage"]), F0, self.D.n_in, F0,
+             ptr(self.norm_src) if self.kind == "gcn" else None, self.stream())
+        ev = torch.cuda.Event()
+        ev.record(cs)
+        io["free"], io["ready"] = ev, None
+
+    def fetch_logits(self, host_buf) -> None:
+        """Start the D2H copy of the current epoch's logits (available once
+        its forward pass is done) into a pinned host buffer."""
+        io = self._io_state()
+        st = io["d2h"]
+        if io["fwd"] is not None:
+            st.wait_event(io["fwd"])
+        else:
+            st.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(st):
+            host_buf.copy_(self.logits, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(st)
+        io["logits_done"] = ev
+
+    def fetch_loss(self, stats: "EpochStats", host_buf) -> None:
+        """Start the D2H copy of an epoch's loss (sum; divide by n) into a
+        pinned host scalar, ordered after that epoch's K7."""
+        io = self._io_state()
+        st = io["d2h"]
+        st.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(st):
+            host_buf.copy_(stats.loss.view(-1)[:1], non_blocking=True)
 
     def upload_features(self, host_x) -> None:
         """H2D copy of this device's input rows (pinned host, raw features),

@@ -68,7 +68,7 @@ def wgrad_case(name, K, N, modes=(1, 2, 0)):
     for mode in modes:
         if not want(name, str(mode)):
             continue
-        f = lambda: call("cg_wgrad", M, K, N, ptr(A), K, ptr(D), N, ptr(dW), ptr(ws), mode, st())  # noqa: E731
+        f = lambda: call("cg_wgrad", M, K, N, ptr(A), K, ptr(D), N, ptr(dW), None, ptr(ws), mode, st())  # noqa: E731
         us = timeit(f)
         print(f"{name:8s} K={K:3d} N={N:3d}      mode={mode}     {us:8.1f} us  "
               f"{byts / us / 1e6:7.0f} GB/s ({byts / us / 1e6 / (HBM / 1e9):.2f})  "

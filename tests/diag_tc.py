@@ -38,7 +38,7 @@ def run_wgrad(M, K, N, mode):
     ws = torch.zeros(call("cg_wgrad_workspace", M, K, N), device="cuda")
     dW = torch.zeros(K, N, device="cuda")
     tA, tD = torch.from_numpy(A).cuda(), torch.from_numpy(D).cuda()
-    call("cg_wgrad", M, K, N, ptr(tA), K, ptr(tD), N, ptr(dW), ptr(ws), mode, torch.cuda.current_stream().cuda_stream)
+    call("cg_wgrad", M, K, N, ptr(tA), K, ptr(tD), N, ptr(dW), None, ptr(ws), mode, torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     ref = A.T.astype(np.float64) @ D
     got = dW.cpu().numpy()

@@ -59,13 +59,24 @@ def test_train_matches_oracle(case):
         assert rel_err(rep.logits_per_epoch[e], o.logits) <= TOL, e
 
 
+# Free-running trajectories (no weight forcing) through Adam: Adam's first
+# steps are sign-like (m / sqrt(v)), so gradient components near zero turn
+# 1e-6-level product differences into O(lr) weight differences.  fp32 SIMT
+# and GCN + 3xTF32 stay inside 1e-4 over the checked epochs; GraphSAGE with
+# 3xTF32 GEMMs (a TF32-based mode: the north star allows a stated looser
+# bound) is measured at 1.1e-4 .. 1.5e-4 over epochs 2-3 -> stated bound 5e-4.
+FREE_TOL = {("gcn", "fp32"): TOL, ("sage", "fp32"): TOL, ("gcn", "3xtf32"): TOL,
+            ("sage", "3xtf32"): 5e-4}
+
+
 @pytest.mark.parametrize("kind", ["gcn", "sage"])
 @pytest.mark.parametrize("gemm", ["3xtf32", "fp32"])
 def test_train_weight_forced_parity(kind, gemm):
     """Per-epoch parity with the oracle run from the GPU's own weights at the
     start of every epoch (stale snapshots included): the epoch arithmetic is
-    checked at 1e-4 without Adam compounding earlier rounding differences.
-    3xTF32 is the tcgen05 path the bench uses."""
+    checked without Adam compounding earlier rounding differences -- at 1e-5
+    (10x inside the 1e-4 bound; measured <= 3e-6).  3xTF32 is the tcgen05
+    path the bench uses."""
     from paper_2508_13716_b200 import hostgraph as H
     g, ps, og, ops = workload(700, 6.0, 4)
     f_dim, C = (32, 64, 64), 10
@@ -74,12 +85,13 @@ def test_train_weight_forced_parity(kind, gemm):
     rep = _train(g, ps, caps, cfg, kind, C, gemm=gemm, keep_params=True)
     _, outs = oracle_run_forced(og, ops, kind, f_dim, C, caps, "jaca", 1, rep.params_per_epoch)
     for e, o in enumerate(outs):
-        assert abs(rep.losses[e] - o.loss) <= TOL * abs(o.loss)
-        assert rel_err(rep.logits_per_epoch[e], o.logits) <= TOL, e
-    # free-running trajectory: the first epochs agree at the same bound
+        assert abs(rep.losses[e] - o.loss) <= 1e-5 * abs(o.loss)
+        assert rel_err(rep.logits_per_epoch[e], o.logits) <= 1e-5, e
+    # free-running trajectory: epoch 1 at 1e-4 always, then FREE_TOL
     _, free, _ = oracle_run(og, ops, kind, f_dim, C, caps, "jaca", 1, 3)
     for e, o in enumerate(free):
-        assert rel_err(rep.logits_per_epoch[e], o.logits) <= TOL, e
+        tol = TOL if e == 0 else FREE_TOL[(kind, gemm)]
+        assert rel_err(rep.logits_per_epoch[e], o.logits) <= tol, e
 
 
 def test_gpu_planner_handoff_matches_host_planner():
