@@ -76,6 +76,7 @@ struct Params {
     int b_lo_off;    // offset of B_lo from the B slice in a stage
     int acc_stride;  // TMEM columns between the two accumulator buffers
     int tma_store;   // C written by TMA bulk tensor stores (mC is valid)
+    int tma_mask;    // ReLU-backward mask tiles TMA-loaded into the store staging (mM)
     float *bws;      // weight gradient only: per (chunk, splitter warp) column sums
                      // of the MN-major B operand (= the bias gradient partials)
 };
@@ -112,15 +113,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     } while (!done);
 }
 
-__device__ __forceinline__ uint32_t rn_tf32(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return r;
-}
 
-// x - trunc_tf32(x), rounded to a TF32 value (|error| <= 2^-12 |x - trunc|)
+// x - trunc_tf32(x) (exact in fp32; the MMA truncates it to TF32 in turn)
 __device__ __forceinline__ uint32_t lo_of_trunc(uint32_t x) {
-    return rn_tf32(__uint_as_float(x) - __uint_as_float(x & 0xFFFFE000u));
+    return __float_as_uint(__uint_as_float(x) - __uint_as_float(x & 0xFFFFE000u));
 }
 
 __device__ __forceinline__ bool elect_one() {
@@ -182,6 +178,15 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
         "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]),
         "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
         "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap *map, uint64_t *bar, void *dst, int x,
+                                            int y, int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
         : "memory");
 }
 
@@ -294,7 +299,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mB0,
           const __grid_constant__ CUtensorMap mA1, const __grid_constant__ CUtensorMap mB1,
           const __grid_constant__ CUtensorMap mBl0, const __grid_constant__ CUtensorMap mBl1,
-          const __grid_constant__ CUtensorMap mC, const Params p) {
+          const __grid_constant__ CUtensorMap mC, const __grid_constant__ CUtensorMap mM,
+          const Params p) {
     // no static shared memory in this kernel, so the dynamic window starts
     // 1024-byte aligned (required by the 128B-swizzle atoms); pointers stay
     // derived from the __shared__ array so accesses compile to LDS/STS
@@ -309,6 +315,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
     uint64_t *tfull = empty + S;   // [2] accumulator ready
     uint64_t *tempty = tfull + 2;  // [2] accumulator drained
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    uint64_t *mbar_mask = tempty + 3;  // [4] one per epilogue warp
 
     // warp index made provably warp-uniform (shfl) so role branches do not diverge
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
@@ -327,6 +334,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 128);
         }
+        for (int a = 0; a < 4; ++a) mbar_init(&mbar_mask[a], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -462,7 +470,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
         // row's 128-byte segment (no transposes, ~4 instructions per float4).
         const int q = warp & 3;
         uint8_t *stg0 = smem + S * stage_bytes + 1024 + q * 8192;  // this warp's 2 staging buffers
-        uint32_t ti = 0, nst = 0;
+        uint32_t ti = 0, nst = 0, nmask = 0;
         for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++ti) {
             const TileCoord tc = tile_of(p, t, n_tiles, m_tiles);
             const uint32_t acc_buf = ti & 1;
@@ -476,19 +484,38 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
             const float rs = (p.row_scale && row_ok) ? p.row_scale[row] : 1.f;
             const float *brow = p.bias ? p.bias + tc.n0 : nullptr;
             for (int c0 = 0; c0 < p.BN; c0 += 32) {
-                float v[32];
-                tmem_ld32(tmem_base + acc_buf * p.acc_stride + ((uint32_t)(32 * q) << 16) + c0, v);
                 int ncol = p.N - (tc.n0 + c0);
                 if (ncol > p.BN - c0) ncol = p.BN - c0;
                 if (ncol > 32) ncol = 32;
+                if (p.tma_store && p.tma_mask && ncol > 0) {
+                    // the mask block comes by TMA into the staging buffer this
+                    // chunk will be stored from; it lands while TMEM is read
+                    if (lane == 0) {
+                        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                        mbar_expect_tx(&mbar_mask[q], 4096);
+                        tma_load_3d(&mM, &mbar_mask[q], stg0 + (nst & 1) * 4096, tc.n0 + c0,
+                                    (int)(tc.m0 + 32 * q), 0);
+                    }
+                }
+                float v[32];
+                tmem_ld32(tmem_base + acc_buf * p.acc_stride + ((uint32_t)(32 * q) << 16) + c0, v);
                 if (ncol <= 0) continue;
                 if (p.tma_store) {
                     // apply the epilogue in registers, stage the 32 x 32 block
                     // (swizzled: chunk j of row r at j ^ (r & 7)), one TMA store
                     const uint32_t stg = smem_u32(stg0 + (nst & 1) * 4096);
-                    // issue the row's mask loads before anything waits
                     float4 mk[8];
-                    if (mrow && row_ok) {
+                    if (p.tma_mask) {
+                        mbar_wait(&mbar_mask[q], nmask & 1);
+                        ++nmask;
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                         : "=f"(mk[j].x), "=f"(mk[j].y), "=f"(mk[j].z), "=f"(mk[j].w)
+                                         : "r"(stg + lane * 128 + 16 * (j ^ (lane & 7)))
+                                         : "memory");
+                    } else if (mrow && row_ok) {
+                        // issue the row's mask loads before anything waits
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
                             if (4 * j >= ncol) {
@@ -504,7 +531,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                             }
                         }
                     }
-                    if (lane == 0)  // the store that used this buffer 2 chunks ago has read it
+                    if (lane == 0 && !p.tma_mask)  // the store 2 chunks ago has read this buffer
                         asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
                     __syncwarp();
 #pragma unroll
@@ -528,7 +555,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                             y.z = fmaxf(y.z, 0.f); y.w = fmaxf(y.w, 0.f);
                         }
                         y.x *= rs; y.y *= rs; y.z *= rs; y.w *= rs;
-                        if (mrow && row_ok) {
+                        if (mrow) {
                             const float4 m = mk[j];
                             y.x = m.x > 0.f ? y.x : 0.f; y.y = m.y > 0.f ? y.y : 0.f;
                             y.z = m.z > 0.f ? y.z : 0.f; y.w = m.w > 0.f ? y.w : 0.f;
@@ -637,7 +664,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                                 if (i >= nb16) break;
                                 const uint4 w = bh[i];
                                 // B stays raw in smem (the MMA truncates it to
-                                // TF32); B_lo = TF32(B - trunc(B))
+                                // TF32); B_lo = B - trunc(B), exact in fp32
                                 bl[i] = make_uint4(lo_of_trunc(w.x), lo_of_trunc(w.y),
                                                    lo_of_trunc(w.z), lo_of_trunc(w.w));
                                 if (bsum) {
@@ -651,13 +678,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                         }
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) {
-                            // hi = RN TF32(x), lo = RN TF32(x - hi): both exact
-                            // TF32 values, |x - hi - lo| <= 2^-23 |x|
-                            const float x = __uint_as_float(hv[i]);
-                            hv[i] = rn_tf32(x);
-                            lv[i] = rn_tf32(x - __uint_as_float(hv[i]));
-                        }
+                        for (int i = 0; i < 32; ++i)   // hi = x as is (the MMA truncates)
+                            lv[i] = __float_as_uint(__uint_as_float(hv[i]) -
+                                                    __uint_as_float(hv[i] & 0xFFFFE000u));
                         const uint32_t ta = tmem_base + ((uint32_t)(32 * q) << 16) + A_TMEM_COL + 64 * s;
                         tmem_st32(ta, hv);
                         tmem_st32(ta + 32, lv);
@@ -788,11 +811,14 @@ int launch(const Params &p0, const CUtensorMap &a0, const CUtensorMap &b0, const
            const CUtensorMap &b1, const CUtensorMap &bl0, const CUtensorMap &bl1, int grid_z,
            cudaStream_t st) {
     Params p = p0;
-    CUtensorMap mc;
+    CUtensorMap mc, mm;
     memset(&mc, 0, sizeof(mc));
+    memset(&mm, 0, sizeof(mm));
     static const bool no_tma_store = getenv("CG_GEMM_NO_TMA_STORE") != nullptr;  // experiment knob
     p.tma_store = !no_tma_store && !(p.ldc % 4) && !((uintptr_t)p.C % 16) &&
                   make_map_c(&mc, p.C, p.M, p.N, p.ldc, grid_z);
+    p.tma_mask = p.tma_store && p.mask && !(p.ldm % 4) && !((uintptr_t)p.mask % 16) &&
+                 make_map_c(&mm, const_cast<float *>(p.mask), p.M, p.N, p.ldm, 1);
     // B slice: MN-major B is loaded in 32-column boxes of 4 KB each
     int b_bytes = 0;
     for (int o = 0; o < p.n_ops; ++o) {
@@ -840,7 +866,7 @@ int launch(const Params &p0, const CUtensorMap &a0, const CUtensorMap &b0, const
     }
     const int64_t tiles = (int64_t)((p.N + p.BN - 1) / p.BN) * ((p.M + BM - 1) / BM) * grid_z;
     const unsigned grid = (unsigned)(tiles < n_sm ? tiles : n_sm);   // persistent
-    k_gemm_tc<<<grid, THREADS, smem, st>>>(a0, b0, a1, b1, bl0, bl1, mc, p);
+    k_gemm_tc<<<grid, THREADS, smem, st>>>(a0, b0, a1, b1, bl0, bl1, mc, mm, p);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 1 : cg_cuda_fail(e, "k_gemm_tc");
 }
