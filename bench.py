@@ -35,11 +35,34 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# BASELINE.json configs (C2 is the default bench line; C3 / C4 are extra
+# measurement runs of the larger shapes, selected with --config)
+CONFIGS = {
+    "c2": dict(n=169343, e=1166244, f_dim=(128, 256, 256), classes=40, model="gcn", hops=1,
+               workload="C2 ogbn-arxiv-shaped ER graph 169,343 v / 1,166,244 e, GCN 3-layer "
+                        "f_dim (128,256,256) -> 40 classes, P=8 random partitions, JACA "
+                        "Algorithm-1 capacities (180 GiB HBM, 64 GiB host), staleness -1"),
+    "c4": dict(n=2449029, e=61859140, f_dim=(100, 256, 256), classes=47, model="gcn", hops=1,
+               workload="C4 ogbn-products-shaped ER graph 2,449,029 v / 61,859,140 e, GCN "
+                        "3-layer f_dim (100,256,256) -> 47 classes, P=8 partitions (random; "
+                        "RAPA on identical B200 profiles only permutes slots), JACA "
+                        "Algorithm-1 capacities (180 GiB HBM, 64 GiB host), staleness -1"),
+    "c3": dict(n=232965, e=114615892, f_dim=(604, 256), classes=41, model="sage", hops=2,
+               workload="C3 Reddit-shaped ER graph 232,965 v / 114,615,892 e, GraphSAGE-mean "
+                        "2-layer f_dim (602 padded to 604, 256) -> 41 classes, 2-hop halos, "
+                        "P=8 random partitions, JACA Algorithm-1 capacities, staleness -1"),
+}
 N_C2, E_C2 = 169343, 1166244
-F_DIM, CLASSES, PARTS = (128, 256, 256), 40, 8
-WORKLOAD = ("C2 ogbn-arxiv-shaped ER graph 169,343 v / 1,166,244 e, GCN 3-layer "
-            "f_dim (128,256,256) -> 40 classes, P=8 random partitions, JACA Algorithm-1 "
-            "capacities (180 GiB HBM, 64 GiB host), staleness -1")
+F_DIM, CLASSES, PARTS, MODEL, HOPS = (128, 256, 256), 40, 8, "gcn", 1
+WORKLOAD = CONFIGS["c2"]["workload"]
+CONFIG = "c2"
+
+
+def apply_config(name: str) -> None:
+    global N_C2, E_C2, F_DIM, CLASSES, MODEL, HOPS, WORKLOAD, CONFIG
+    c = CONFIGS[name]
+    N_C2, E_C2, F_DIM, CLASSES = c["n"], c["e"], c["f_dim"], c["classes"]
+    MODEL, HOPS, WORKLOAD, CONFIG = c["model"], c["hops"], c["workload"], name
 
 
 def peaks():
@@ -99,8 +122,9 @@ class ClockSampler:
 def build_workload(parts: int):
     from paper_2508_13716_b200 import hostgraph as H
     g = H.erdos_renyi(N_C2, E_C2 / N_C2, 0)
-    ps = H.build_partition_set(g, H.random_partition(N_C2, parts, 0), 1)
-    caps = H.compute_capacities(ps, -1, [180.0] * parts, 1024.0, 64.0, 2048.0, F_DIM, 3)
+    ps = H.build_partition_set(g, H.random_partition(N_C2, parts, 0), HOPS)
+    caps = H.compute_capacities(ps, -1, [180.0] * parts, 1024.0, 64.0, 2048.0, F_DIM,
+                                len(F_DIM))
     return g, ps, caps
 
 
@@ -125,7 +149,7 @@ def run_ours(args):
     cfg = H.SimConfig(epochs=args.warmup + args.steps, policy="jaca",
                       staleness_bound=args.staleness, f_dim=F_DIM, L=len(F_DIM))
     # the public drop-in, stepwise: same setup as api.train()
-    sess = api.TrainSession(g, ps, H.unit_profiles(args.parts), caps, cfg, model="gcn",
+    sess = api.TrainSession(g, ps, H.unit_profiles(args.parts), caps, cfg, model=MODEL,
                             num_classes=CLASSES, gemm=args.gemm, keep_logits="none")
     eng = sess.engine
     t_setup = time.perf_counter() - t_setup
@@ -236,7 +260,12 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(g, ps, caps, budget_s=args.cpu_budget)
+        if CONFIG == "c2":
+            cpu = cpu_baseline(g, ps, caps, budget_s=args.cpu_budget)
+        else:
+            cpu = {"value": None, "unit": "GTEPS", "cores": len(os.sched_getaffinity(0)),
+                   "kind": "port", "sample": "not run: one oracle-port epoch of this shape "
+                   "exceeds the bench's few-minute budget (see the C2 line)"}
     sess.close()
     if rank == 0:
         line = {
@@ -295,10 +324,10 @@ class OracleSession:
         dims = list(F_DIM) + [CLASSES]
         self.planner = ohp.Planner("jaca", (caps.c_cpu, tuple(caps.c_gpu),
                                             caps.bytes_per_entry), ranked, ps.halo, imp)
-        self.trainer = omp.Trainer(og, ps.inner, ps.halo, omp.ModelSpec("gcn", dims),
+        self.trainer = omp.Trainer(og, ps.inner, ps.halo, omp.ModelSpec(MODEL, dims),
                                    omp.features(g.n_vertices, F_DIM[0], 0),
                                    omp.labels(g.n_vertices, CLASSES, 1),
-                                   params=omp.init_params("gcn", dims, 2))
+                                   params=omp.init_params(MODEL, dims, 2))
         self.s = staleness
         self.e = 0
         self.n_edges = g.n_edges
@@ -367,12 +396,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--parts", type=int, default=PARTS)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--staleness", type=int, default=-1)
     ap.add_argument("--gemm", default="3xtf32", choices=["fp32", "3xtf32", "tf32"])
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-budget", type=float, default=150.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    apply_config(args.config)
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
