@@ -204,6 +204,8 @@ def run_ours(args):
     try:
         with open(os.path.join(ROOT, "profiles", "spmm_traffic.json")) as fh:
             prof = json.load(fh)
+        if prof.get("config", "c2") != CONFIG:
+            prof = {}   # the committed ncu capture is of another workload
     except Exception:  # noqa: BLE001
         pass
 

@@ -94,7 +94,7 @@ def main(src: str, dst: str):
         if name == "prof_spmm" and rows:
             tot = sum(r.get("dram_read_B", 0) + r.get("dram_write_B", 0) for r in rows)
             dur = sum(r.get("duration_s", 0) for r in rows)
-            traffic = {"source": f"{dst}/ncu_{name}.csv",
+            traffic = {"source": f"{dst}/ncu_{name}.csv", "config": "c2",
                        "launches": len(rows),
                        "dram_bytes_per_epoch": tot,
                        "dram_bytes_per_launch": tot / len(rows),
