@@ -1,0 +1,106 @@
+"""Artifact I/O and the CLI (train = drop-in for `halopart simulate`).
+
+CPU: the readers against the reference-produced fixtures in tests/golden/cli
+(tests/golden/make_cli_golden.py ran the reference CLI).  GPU: `train` on the
+same inputs emits sim_report.json / .csv byte-identical to the reference's.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import io
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from paper_2508_13716_b200 import artifacts as A
+from paper_2508_13716_b200 import cli
+from paper_2508_13716_b200 import hostgraph as H
+from paper_2508_13716_b200.errors import DomainError, ParseError
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = os.path.join(ROOT, "tests", "golden", "cli")
+
+
+def _exp():
+    with open(os.path.join(GOLD, "expected.json")) as fh:
+        return json.load(fh)
+
+
+def test_edge_list_matches_generator():
+    g = A.load_edge_list(os.path.join(GOLD, "graph.txt"))
+    ref = H.erdos_renyi(400, 8.0, 3)
+    assert g.n_vertices == 400 and g.n_edges == ref.n_edges
+    for k in ("out_offsets", "out_targets", "in_offsets", "in_targets"):
+        assert np.array_equal(getattr(g, k), getattr(ref, k)), k
+
+
+def test_edge_list_semantics():
+    g = A.load_edge_list(io.StringIO("# c\n0 1\n0 1\n\n1 1\n2 0\n"))
+    assert g.n_vertices == 3 and g.n_edges == 3          # duplicate collapsed, self-loop kept
+    with pytest.raises(DomainError):
+        A.load_edge_list(io.StringIO("0 5\n"))            # gap without compact_ids
+    g2 = A.load_edge_list(io.StringIO("10 50\n50 70\n"), compact_ids=True)
+    assert g2.n_vertices == 3 and g2.vertex_id_map == {10: 0, 50: 1, 70: 2}
+    for bad in ("0 1 2\n", "a b\n", "-1 2\n"):
+        with pytest.raises(ParseError):
+            A.load_edge_list(io.StringIO(bad))
+
+
+def test_rapa_import_and_profiles():
+    exp = _exp()
+    res, ps = A.import_rapa_result(os.path.join(GOLD, "rapa.json"))
+    assert list(res.sigma) == exp["sigma"] and res.feasible == exp["feasible"]
+    assert [h.size for h in ps.halo] == exp["halo_sizes"]
+    assert sum(a.size for a in ps.inner) == 400
+    prof = A.load_device_profiles(os.path.join(GOLD, "devices.json"))
+    assert [p.id for p in prof] == ["3090-a", "3090-b", "3060-a", "3060-b"]
+    with pytest.raises(ParseError):
+        A.load_device_profiles(io.StringIO("[]"))
+    with pytest.raises(DomainError):
+        A.load_device_profiles(io.StringIO('[{"id": "x", "mm_s": 0, "spmm_s": 1, "h2d_s": 1, '
+                                           '"d2h_s": 1, "idt_s": 1, "mem_gb": 1}]'))
+
+
+def test_cli_option_precedence(tmp_path):
+    cfgf = tmp_path / "c.json"
+    cfgf.write_text(json.dumps({"epochs": 7, "policy": "lru"}))
+    args = cli.build_parser().parse_args(["train", "--config", str(cfgf), "--policy", "fifo"])
+    opts = cli._resolve(args, cli._TRAIN_DEFAULTS)
+    assert opts["epochs"] == 7 and opts["policy"] == "fifo" and opts["staleness"] == -1
+    cfgf.write_text(json.dumps({"bogus": 1}))
+    with pytest.raises(ParseError):
+        cli._resolve(args, cli._TRAIN_DEFAULTS)
+    assert cli.main(["train"]) == 2                      # missing --graph: exit 2
+
+
+@pytest.mark.gpu
+def test_cli_train_reproduces_reference_sim_report(tmp_path):
+    exp = _exp()
+    out = tmp_path / "run"
+    cmd = [sys.executable, "-m", "paper_2508_13716_b200.cli", "train",
+           "--graph", os.path.join(GOLD, "graph.txt"),
+           "--partition-result", os.path.join(GOLD, "rapa.json"),
+           "--devices", os.path.join(GOLD, "devices.json"), *exp["sim_flags"],
+           "--classes", "7", "--trace", "--out", str(out)]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    sha = lambda p: hashlib.sha256((out / p).read_bytes()).hexdigest()  # noqa: E731
+    assert sha("sim_report.json") == exp["sim_report_json_sha256"]
+    assert sha("sim_report.csv") == exp["sim_report_csv_sha256"]
+    tr = json.loads((out / "train_report.json").read_text())
+    assert len(tr["losses"]) == 5 and all(np.isfinite(tr["losses"]))
+    man = json.loads((out / "manifest.json").read_text())
+    assert man["outputs"][-1] == "manifest.json" and "trace.csv" in man["outputs"]
+
+
+@pytest.mark.gpu
+def test_cli_profile_rows_load(tmp_path):
+    out = tmp_path / "devices.json"
+    assert cli.main(["profile", "--n", "2048", "--reps", "3", "--out", str(out)]) == 0
+    rows = A.load_device_profiles(out)
+    assert rows and all(p.mm_s > 0 and p.mem_gb > 1 for p in rows)
