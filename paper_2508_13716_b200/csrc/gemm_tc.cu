@@ -40,9 +40,9 @@ constexpr int UK = 8;            // K per tcgen05.mma kind::tf32
 constexpr int BN_MAX = 256;     // TMEM columns per accumulator buffer (1xTF32 tiles)
 constexpr int BN_MAX_3X = 128;  // 3xTF32 tiles: smaller B slices buy a deeper stage ring
 constexpr int A_BYTES = BM * BK * 4;             // 16 KB A operand stage
-constexpr int EPI_BYTES = 4 * 2 * 4096;     // per epilogue warp: 2 x (32 rows x 128 B) TMA-store staging
+constexpr int EPI_BUF = 4096;               // one 32 rows x 128 B TMA staging buffer
 constexpr int SMEM_LIMIT = 227 * 1024;
-constexpr int SMEM_FIXED = 1024 + EPI_BYTES;  // barriers, epilogue staging
+constexpr int SMEM_BARS = 1024;              // mbarriers + TMEM slot
 // Stage layout: [A | B] (hi) and, for 3xTF32, [A_lo | B_lo] at +hi_bytes.
 constexpr int THREADS = 384;  // 12 warps: TMA, MMA, -, -, 4 epilogue, 4 splitter
 
@@ -77,6 +77,7 @@ struct Params {
     int acc_stride;  // TMEM columns between the two accumulator buffers
     int tma_store;   // C written by TMA bulk tensor stores (mC is valid)
     int tma_mask;    // ReLU-backward mask tiles TMA-loaded into the store staging (mM)
+    int nbuf;        // staging buffers per epilogue warp (2, or 4 to prefetch masks)
     float *bws;      // weight gradient only: per (chunk, splitter warp) column sums
                      // of the MN-major B operand (= the bias gradient partials)
 };
@@ -315,7 +316,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
     uint64_t *tfull = empty + S;   // [2] accumulator ready
     uint64_t *tempty = tfull + 2;  // [2] accumulator drained
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
-    uint64_t *mbar_mask = tempty + 3;  // [4] one per epilogue warp
+    uint64_t *mbar_mask = tempty + 3;  // [4 warps][nbuf] mask-tile arrivals
 
     // warp index made provably warp-uniform (shfl) so role branches do not diverge
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
@@ -334,7 +335,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 128);
         }
-        for (int a = 0; a < 4; ++a) mbar_init(&mbar_mask[a], 1);
+        for (int a = 0; a < 4 * p.nbuf; ++a) mbar_init(&mbar_mask[a], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -469,8 +470,37 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
         // / row scale / ReLU-backward mask -> eight 16-byte stores of the
         // row's 128-byte segment (no transposes, ~4 instructions per float4).
         const int q = warp & 3;
-        uint8_t *stg0 = smem + S * stage_bytes + 1024 + q * 8192;  // this warp's 2 staging buffers
-        uint32_t ti = 0, nst = 0, nmask = 0;
+        const int NB = p.nbuf;
+        uint8_t *stg0 = smem + S * stage_bytes + SMEM_BARS + q * NB * EPI_BUF;  // NB buffers
+        uint64_t *mbq = mbar_mask + q * NB;
+        uint32_t ti = 0, nst = 0;
+        // Mask prefetch cursor over this warp's (tile, chunk) sequence, valid
+        // chunks only: masks run D = NB - 2 chunks ahead of the one consumed,
+        // so the buffer a prefetch lands in was last stored from two chunks
+        // before the current one (wait_group.read 1 frees it).
+        const int D = NB - 2;
+        int64_t pf_t = blockIdx.x;
+        int pf_c = 0;
+        uint32_t pf_k = 0;
+        auto pf_issue = [&]() -> bool {
+            if (pf_t >= total_tiles) return false;   // sequence exhausted
+            const TileCoord pc = tile_of(p, pf_t, n_tiles, m_tiles);
+            if (lane == 0) {
+                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                uint64_t *bar = &mbq[pf_k % NB];
+                mbar_expect_tx(bar, EPI_BUF);
+                tma_load_3d(&mM, bar, stg0 + (pf_k % NB) * EPI_BUF, pc.n0 + 32 * pf_c,
+                            (int)(pc.m0 + 32 * q), 0);
+            }
+            ++pf_k;
+            // advance to the next chunk with columns left
+            while (true) {
+                if (++pf_c * 32 >= p.BN) { pf_c = 0; pf_t += gridDim.x; }
+                if (pf_t >= total_tiles) break;
+                if (p.N - (tile_of(p, pf_t, n_tiles, m_tiles).n0 + 32 * pf_c) > 0) break;
+            }
+            return true;
+        };
         for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++ti) {
             const TileCoord tc = tile_of(p, t, n_tiles, m_tiles);
             const uint32_t acc_buf = ti & 1;
@@ -488,14 +518,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                 if (ncol > p.BN - c0) ncol = p.BN - c0;
                 if (ncol > 32) ncol = 32;
                 if (p.tma_store && p.tma_mask && ncol > 0) {
-                    // the mask block comes by TMA into the staging buffer this
-                    // chunk will be stored from; it lands while TMEM is read
-                    if (lane == 0) {
-                        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-                        mbar_expect_tx(&mbar_mask[q], 4096);
-                        tma_load_3d(&mM, &mbar_mask[q], stg0 + (nst & 1) * 4096, tc.n0 + c0,
-                                    (int)(tc.m0 + 32 * q), 0);
-                    }
+                    // mask blocks come by TMA into the staging buffers the
+                    // chunks will be stored from, D chunks ahead
+                    while (pf_k <= nst + D && pf_issue()) {}
                 }
                 float v[32];
                 tmem_ld32(tmem_base + acc_buf * p.acc_stride + ((uint32_t)(32 * q) << 16) + c0, v);
@@ -503,11 +528,10 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                 if (p.tma_store) {
                     // apply the epilogue in registers, stage the 32 x 32 block
                     // (swizzled: chunk j of row r at j ^ (r & 7)), one TMA store
-                    const uint32_t stg = smem_u32(stg0 + (nst & 1) * 4096);
+                    const uint32_t stg = smem_u32(stg0 + (nst % NB) * EPI_BUF);
                     float4 mk[8];
                     if (p.tma_mask) {
-                        mbar_wait(&mbar_mask[q], nmask & 1);
-                        ++nmask;
+                        mbar_wait(&mbq[nst % NB], (nst / NB) & 1);
 #pragma unroll
                         for (int j = 0; j < 8; ++j)
                             asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -531,7 +555,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                             }
                         }
                     }
-                    if (lane == 0 && !p.tma_mask)  // the store 2 chunks ago has read this buffer
+                    if (lane == 0 && !p.tma_mask)  // the store NB chunks ago has read this buffer
                         asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
                     __syncwarp();
 #pragma unroll
@@ -568,7 +592,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     __syncwarp();
                     if (lane == 0)
-                        tma_store_3d(&mC, stg0 + (nst & 1) * 4096, tc.n0 + c0,
+                        tma_store_3d(&mC, stg0 + (nst % NB) * EPI_BUF, tc.n0 + c0,
                                      (int)(tc.m0 + 32 * q), tc.z);
                     ++nst;
                     continue;
@@ -840,7 +864,10 @@ int launch(const Params &p0, const CUtensorMap &a0, const CUtensorMap &b0, const
         p.acc_stride = BN_MAX;
     }
     const int stage_bytes = p.stage_bytes;
-    int stages = (SMEM_LIMIT - SMEM_FIXED) / stage_bytes;
+    // masked epilogues prefetch their mask tiles: 4 staging buffers per warp
+    p.nbuf = p.tma_mask ? 4 : 2;
+    const int smem_fixed = SMEM_BARS + 4 * p.nbuf * EPI_BUF;
+    int stages = (SMEM_LIMIT - smem_fixed) / stage_bytes;
     static const int env_stages = getenv("CG_GEMM_STAGES") ? atoi(getenv("CG_GEMM_STAGES")) : 0;
     int cap = env_stages > 0 ? env_stages : 6;   // experiment knob
     if (p.a_tmem && cap > 4) cap = 4;            // TMEM: 2 x 128 accumulator + 4 x 64 A columns
@@ -849,7 +876,7 @@ int launch(const Params &p0, const CUtensorMap &a0, const CUtensorMap &b0, const
         cg_set_error("k_gemm_tc: stage does not fit shared memory");
         return -1;
     }
-    const size_t smem = (size_t)p.stages * stage_bytes + SMEM_FIXED;
+    const size_t smem = (size_t)p.stages * stage_bytes + smem_fixed;
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
