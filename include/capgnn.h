@@ -164,6 +164,10 @@ typedef struct cg_plan_static {
     int32_t gfree;              /* admit mode of the global level          */
     int32_t policy;             /* 0 jaca, 1 fifo                          */
     int32_t n_parts;
+    const int32_t *req_snap;    /* absolute epoch-1 snapshot row of the
+                                   requester's vertex on its device, or -1:
+                                   every read at version <= 1 is served
+                                   from it; NULL = none      */
 } cg_plan_static;
 
 int cg_plan_frozen(const cg_plan_static *st, int epoch, int staleness, int me,

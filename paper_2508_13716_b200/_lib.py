@@ -27,7 +27,8 @@ class PlanStatic(C.Structure):
     _fields_ = [("n_union", I64), ("req_off", P), ("req_part", P), ("req_dev", P),
                 ("req_pos", P), ("req_slot", P), ("req_needed", P), ("owner_dev", P),
                 ("owner_row", P), ("gslot", P), ("lfree", P), ("score", P), ("lmin", P),
-                ("gmin", F64), ("gfree", I32), ("policy", I32), ("n_parts", I32)]
+                ("gmin", F64), ("gfree", I32), ("policy", I32), ("n_parts", I32),
+                ("req_snap", P)]
 
 
 # name -> argtypes (restype int unless listed in _RESTYPES)

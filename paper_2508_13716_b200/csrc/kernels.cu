@@ -580,6 +580,12 @@ __device__ __forceinline__ void plan_vertex(const cg_plan_static &st, int64_t u,
             stage_src[pos] = -1;
             continue;
         }
+        if (st.req_snap && ver <= 1) {
+            // version 0/1 = the epoch-1 activation: the shared snapshot row
+            halo_row[pos] = st.req_snap[k];
+            stage_src[pos] = -1;
+            continue;
+        }
         if (oc == 0 && !cur) {  // stale local hit: read the slab in place
             halo_row[pos] = slot;
             stage_src[pos] = -1;

@@ -177,6 +177,11 @@ class Engine:
         self.b_row = _dev(D.bwd_src_row if n_bwd else [0], i32, dev)
         self.b_dst = _dev(D.n_in + np.arange(nb), i32, dev)
         self.n_bwd = n_bwd
+        # epoch-1 snapshot fill lists (owner device, owner row) -> snap row
+        if D.n_snap:
+            self.snap_src = _dev(D.snap_src_dev, i32, dev)
+            self.snap_srow = _dev(D.snap_src_row, i32, dev)
+            self.snap_dst = _dev(D.snap_off + np.arange(D.n_snap), i32, dev)
         # host tier (global cache level): c_cpu slots x bpe
         self.c_cpu = int(caps.c_cpu)
         self.host = HostTier(self.c_cpu * self.bpe_f * 4, self.comm)
@@ -278,14 +283,17 @@ class Engine:
                 odev = L.owner_dev[k]
                 orow = L.owner_row[k]
                 pos = hp + np.arange(eidx - b)
+                # version <= 1 -> the epoch-1 value: the shared snapshot row
+                ver1 = (np.maximum(ver, 1) == 1) & need
+                halo_row[pos[ver1]] = D.snap_row_of_pos[pos[ver1]]
                 # stale local hit -> read the slab slot in place
-                st_loc = (oc == 0) & ~cur & need
+                st_loc = (oc == 0) & ~cur & need & ~ver1
                 halo_row[pos[st_loc]] = D.slab_off[p] + plan.hit_slot[b:eidx][st_loc]
                 # co-resident owner, current value -> read the owner row in place
-                direct = cur & need & (odev == me)
+                direct = cur & need & (odev == me) & ~ver1
                 halo_row[pos[direct]] = orow[direct]
                 # everything else is staged into its staging row
-                stg = need & ~st_loc & ~direct
+                stg = need & ~st_loc & ~direct & ~ver1
                 halo_row[pos[stg]] = n_in + pos[stg]
                 s_dst[pos[stg]] = n_in + pos[stg]
                 from_owner = stg & cur
@@ -297,16 +305,15 @@ class Engine:
                     raise RuntimeError("stale global hit without a global slot")
                 s_src[pos[from_host]] = nd
                 s_row[pos[from_host]] = gsl
-                # write-back of the final local-slot contents (after the SpMM)
+                # write-back of the final local-slot contents (after the SpMM);
+                # slots at version <= 1 are never read (the snapshot serves them)
                 lo, c = int(self.planner.lslot_off[p]), int(self.planner.c_gpu[p])
                 lpos = plan.lslot_pos[lo:lo + c]
                 dirty = plan.lslot_dirty[lo:lo + c].astype(bool)
-                if e == 1:
-                    dirty |= lpos >= 0   # warm (version 0) entries materialise now
                 sl = np.flatnonzero(dirty & (lpos >= 0))
                 if sl.size:
                     j = lpos[sl]
-                    keep = need[j]
+                    keep = need[j] & (np.maximum(ver[j], 1) > 1)
                     sl, j = sl[keep], j[keep]
                     wb_dst.append(D.slab_off[p] + sl)
                     wb_src.append(halo_row[hp + j])
@@ -314,9 +321,9 @@ class Engine:
         gw = np.full(max(L.union.size if L.union is not None else 0, 1), -1, np.int32)
         if self.c_cpu and L.union is not None and L.union.size:
             gv = plan.gslot_vertex
-            dirty = plan.gslot_dirty.astype(bool)
-            if e == 1:
-                dirty |= gv >= 0
+            # global entries at version <= 1 are served by the snapshot: the
+            # host tier only needs contents written at epoch >= 2
+            dirty = plan.gslot_dirty.astype(bool) & (e > 1)
             sl = np.flatnonzero(dirty & (gv >= 0))
             kk = gv[sl]
             mine = L.owner_dev[kk] == me
@@ -364,13 +371,18 @@ class Engine:
             flag=torch.zeros(1, dtype=i32, device=dev),
             outcome=torch.zeros(max(idx.size, 1), dtype=torch.int8, device=dev))
         k = self.k6
+        mine = L.req_dev == self.me
+        req_snap = np.full(idx.size, -1, np.int32)
+        req_snap[mine] = self.D.snap_row_of_pos[L.req_pos[mine]]
+        k["req_snap"] = _dev(req_snap if req_snap.size else [-1], i32, dev)
         self.k6_static = PlanStatic(
             n_union=int(L.union.size), req_off=ptr(k["req_off"]), req_part=ptr(k["req_part"]),
             req_dev=ptr(k["req_dev"]), req_pos=ptr(k["req_pos"]), req_slot=ptr(k["req_slot"]),
             req_needed=ptr(k["req_needed"]), owner_dev=ptr(k["owner_dev"]),
             owner_row=ptr(k["owner_row"]), gslot=ptr(k["gslot"]), lfree=ptr(k["lfree"]),
             score=ptr(k["score"]), lmin=ptr(k["lmin"]), gmin=float(stt["gmin"]),
-            gfree=int(stt["gfree"]), policy=0 if self.policy == "jaca" else 1, n_parts=L.P)
+            gfree=int(stt["gfree"]), policy=0 if self.policy == "jaca" else 1, n_parts=L.P,
+            req_snap=ptr(k["req_snap"]))
         self.gpu_plan_ready = True
 
     def plan(self, e: int) -> tuple[str, np.ndarray | None, EpochPlan | None]:
@@ -431,6 +443,10 @@ class Engine:
             if l > 0:
                 self.comm.barrier()
                 self._gw(l - 1)
+            if e == 1 and D.n_snap:
+                # epoch-1 snapshot of every halo vertex read on this device
+                self._copy(D.n_snap, F, self.snap_src, self.snap_srow, self.snap_dst,
+                           self.tab[l], self.tab_ld[l], self.X[l], F)
             if D.n_halo:
                 self._copy(D.n_halo, F, self.stage_src, self.stage_row, self.stage_dst,
                            self.tab[l], self.tab_ld[l], self.X[l], F)

@@ -12,7 +12,14 @@ Per device, every layer's activations live in one "extended row space"
                 ascending id) -- what peers read over NVLink;
   staging rows  one per (partition, halo vertex) position, ascending id
                 (the reference's lookup order, simulator.py:198);
-  slab rows     the partitions' local cache levels (c_gpu[p] slots each).
+  slab rows     the partitions' local cache levels (c_gpu[p] slots each);
+  snap rows     one row per distinct halo vertex the device's SpMMs read: the
+                epoch-1 activation of that vertex.  Any cache row whose
+                version is <= 1 holds exactly that value (A2: version 0/1 ->
+                the epoch-1 forward pass), whichever partition's level holds
+                it, so such reads are served from one shared row instead of
+                P per-partition copies (fewer distinct HBM rows per gather,
+                no epoch-1 warm write-back, no host-tier traffic for them).
 
 The forward CSR (in-edges of inner rows, + GCN self-loops) has column ids in
 [0, n_in) for rows owned by the same partition and n_in + halo-position for
@@ -54,6 +61,12 @@ class DeviceLayout:
     norm_dst: np.ndarray         # GCN b_v, SAGE 1/d_in(v) per inner row
     nnz_fwd: int = 0
     nnz_bwd: int = 0
+    snap_off: int = 0            # first epoch-1 snapshot row (absolute)
+    n_snap: int = 0
+    snap_vertex: np.ndarray | None = None   # vertex id per snap row (ascending)
+    snap_row_of_pos: np.ndarray | None = None  # per halo position: absolute snap row / -1
+    snap_src_dev: np.ndarray | None = None  # owner device / row of each snap vertex
+    snap_src_row: np.ndarray | None = None
 
 
 @dataclass
@@ -160,6 +173,14 @@ def build_layout(g, inner, halo, c_gpu, n_dev: int, kind: str) -> RunLayout:
             ok = (idx < h.size) & (h[np.minimum(idx, max(h.size - 1, 0))] == nb[sel]) if h.size else np.zeros(sel.size, bool)
             col[sel[ok]] = n_in + hpos_off[p] + idx[ok]
             needed[hpos_off[p] + idx[ok]] = True
+        # epoch-1 snapshot rows: the distinct halo vertices the SpMM reads
+        snap_vertex = np.unique(halo_vertex[needed]) if n_halo else np.zeros(0, np.int64)
+        snap_off = n_rows
+        snap_row_of_pos = np.full(n_halo, -1, np.int64)
+        if n_halo:
+            nd = np.flatnonzero(needed)
+            snap_row_of_pos[nd] = snap_off + np.searchsorted(snap_vertex, halo_vertex[nd])
+        n_rows += snap_vertex.size
         keep = col >= 0   # edges from RAPA-pruned halo vertices are dropped
         col, owner = col[keep], owner[keep]
         fwd_rowptr = np.zeros(n_in + 1, np.int64)
@@ -213,6 +234,10 @@ def build_layout(g, inner, halo, c_gpu, n_dev: int, kind: str) -> RunLayout:
             bwd_stage_vertex=remote, bwd_src_dev=part_dev[parts_of[remote]].astype(np.int32),
             bwd_src_row=row_of[remote].astype(np.int32), needed=needed,
             norm_src=norm_src, norm_dst=norm_dst, nnz_fwd=int(col.size),
+            snap_off=int(snap_off), n_snap=int(snap_vertex.size), snap_vertex=snap_vertex,
+            snap_row_of_pos=snap_row_of_pos.astype(np.int32),
+            snap_src_dev=part_dev[parts_of[snap_vertex]].astype(np.int32),
+            snap_src_row=row_of[snap_vertex].astype(np.int32),
             nnz_bwd=int(bcol.size)))
 
     # ---- requester tables for the plan (halo-union major, lookup order)
