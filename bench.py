@@ -256,7 +256,7 @@ def run_ours(args):
            "d2h_bytes_per_step": int(host_logits[0].numel() * 4 + 4),
            "steps": e2e_steps, "ms_per_step": w_s / e2e_steps * 1e3,
            "how": "api.TrainSession, 2 untimed warm-up steps, then per step: pinned-host input "
-                  "rows H2D (prefetched one step ahead on a copy stream) + GCN row scaling, "
+                  "rows H2D (prefetched one step ahead on a copy stream; GCN: row scaling), "
                   "epoch, logits + loss D2H (overlapping the backward); host wall clock incl. "
                   "final sync"}
 

@@ -399,29 +399,30 @@ k_colsum_partial(int64_t M, int N, const float *__restrict__ D, int64_t ldd,
 // out[i] = sum_c ws[c][i], fixed order: 8 warps stride the chunks (each
 // keeping 4 independent partial sums so the loads pipeline), then a fixed
 // combination of the partials.
-__global__ void __launch_bounds__(256)
+template <int NW>
+__global__ void __launch_bounds__(NW * 32)
 k_reduce_chunks_tree(int64_t n_out, int64_t n_chunks, const float *__restrict__ ws,
                      float *__restrict__ out) {
-    __shared__ float part[8][33];
+    __shared__ float part[NW][33];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t i = blockIdx.x * 32 + lane;
     float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
     if (i < n_out) {
         int64_t c = w;
-        for (; c + 24 < n_chunks; c += 32) {
+        for (; c + 3 * NW < n_chunks; c += 4 * NW) {
             s0 += ws[c * n_out + i];
-            s1 += ws[(c + 8) * n_out + i];
-            s2 += ws[(c + 16) * n_out + i];
-            s3 += ws[(c + 24) * n_out + i];
+            s1 += ws[(c + NW) * n_out + i];
+            s2 += ws[(c + 2 * NW) * n_out + i];
+            s3 += ws[(c + 3 * NW) * n_out + i];
         }
-        for (; c < n_chunks; c += 8) s0 += ws[c * n_out + i];
+        for (; c < n_chunks; c += NW) s0 += ws[c * n_out + i];
     }
     part[w][lane] = (s0 + s1) + (s2 + s3);
     __syncthreads();
     if (w == 0 && i < n_out) {
         float t = 0.f;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) t += part[k][lane];
+        for (int k = 0; k < NW; ++k) t += part[k][lane];
         out[i] = t;
     }
 }
@@ -668,7 +669,13 @@ inline int grid_for(int64_t work, int threads, int max_blocks = 148 * 16) {
 int cg_reduce_chunks(int64_t n_out, int64_t n_chunks, const float *ws, float *out,
                      cudaStream_t st) {
     if (n_out == 0) return 0;
-    k_reduce_chunks_tree<<<(unsigned)((n_out + 31) / 32), 256, 0, st>>>(n_out, n_chunks, ws, out);
+    // many partial rows (split-K chunks x splitter warps): 32 warps share them
+    if (n_chunks > 64)
+        k_reduce_chunks_tree<32><<<(unsigned)((n_out + 31) / 32), 1024, 0, st>>>(n_out, n_chunks,
+                                                                              ws, out);
+    else
+        k_reduce_chunks_tree<8><<<(unsigned)((n_out + 31) / 32), 256, 0, st>>>(n_out, n_chunks,
+                                                                            ws, out);
     CG_CHECK_LAUNCH("k_reduce_chunks_tree");
     return 1;
 }
@@ -782,7 +789,7 @@ int cg_colsum(int64_t M, int N, const float *D, int64_t ldd, float *db, float *w
     dim3 grid((N + 31) / 32, (unsigned)nch);
     cudaStream_t st = (cudaStream_t)stream;
     k_colsum_partial<<<grid, 256, 0, st>>>(M, N, D, ldd, ws);
-    k_reduce_chunks_tree<<<(N + 31) / 32, 256, 0, st>>>(N, nch, ws, db);
+    k_reduce_chunks_tree<8><<<(N + 31) / 32, 256, 0, st>>>(N, nch, ws, db);
     CG_CHECK_LAUNCH("cg_colsum");
     return 2;
 }
