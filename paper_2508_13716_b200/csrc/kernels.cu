@@ -113,6 +113,12 @@ __global__ void k_copy_rows(int64_t n, int F, const int32_t *__restrict__ src_id
 
 // ---------------------------------------------------------------- K1 ------
 
+#ifndef SPMM_UNR1
+#define SPMM_UNR1 4   // rows in flight per lane, one float4 chunk per lane
+#endif
+#ifndef SPMM_UNR2
+#define SPMM_UNR2 4   // rows in flight per lane, two float4 chunks per lane (3 and 8 measured slower)
+#endif
 #ifndef SPMM_MIN_BLOCKS
 #define SPMM_MIN_BLOCKS 1   // measured: forcing 4 blocks (64 regs, spills) is slower
 #endif
@@ -135,7 +141,7 @@ k_spmm(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
        const float *__restrict__ X, int64_t ldx, const float *__restrict__ scale,
        const float *__restrict__ addend, int64_t ld_add, const float *__restrict__ mask,
        int64_t ld_mask, float *__restrict__ out, int64_t ldo) {
-    constexpr int UNR = 4;
+    constexpr int UNR = (NCH == 1) ? SPMM_UNR1 : SPMM_UNR2;   // rows in flight per lane
     const int lane = threadIdx.x & (G - 1);
     const unsigned gmask = (G == 32) ? 0xffffffffu
                                      : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
