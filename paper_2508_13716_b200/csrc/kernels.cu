@@ -119,9 +119,6 @@ __global__ void k_copy_rows(int64_t n, int F, const int32_t *__restrict__ src_id
 #ifndef SPMM_UNR2
 #define SPMM_UNR2 4   // rows in flight per lane, two float4 chunks per lane (3 and 8 measured slower)
 #endif
-#ifndef SPMM_MIN_BLOCKS
-#define SPMM_MIN_BLOCKS 1   // measured: forcing 4 blocks (64 regs, spills) is slower
-#endif
 
 // G lanes per row, NCH float4 chunks per lane (row width F <= 4*G*NCH).
 // Each G-lane group walks rows r, r+ngrp, ... through a 4-stage software
@@ -135,7 +132,7 @@ __global__ void k_copy_rows(int64_t n, int F, const int32_t *__restrict__ src_id
 // inline.  The grid is sized to the resident-block count (persistent), so a
 // group sees many rows and the pipeline stays full.
 template <int G, int NCH>
-__global__ void __launch_bounds__(256, (NCH <= 2 ? SPMM_MIN_BLOCKS : 1))
+__global__ void __launch_bounds__(256)
 k_spmm(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
        const int32_t *__restrict__ col, int64_t n_direct, const int32_t *__restrict__ halo_row,
        const float *__restrict__ X, int64_t ldx, const float *__restrict__ scale,
