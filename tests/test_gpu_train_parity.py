@@ -122,3 +122,57 @@ def test_bitwise_deterministic_reruns():
     assert a.losses == b.losses
     for x, y in zip(a.logits_per_epoch, b.logits_per_epoch):
         assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("kind", ["gcn", "sage"])
+def test_two_hop_halos_match_oracle(kind):
+    """hops = 2 (C3's setting, A7): lookups and model bytes range over the
+    whole 2-hop halo, aggregation uses the 1-hop in-edges it contains."""
+    from paper_2508_13716_b200 import hostgraph as H
+    g, ps, og, ops = workload(400, 4.0, 4, hops=2)
+    assert sum(h.size for h in ps.halo) > sum(
+        H.build_partition_set(g, H.random_partition(400, 4, 0), 1).halo_sizes)
+    f_dim, C = (16, 32), 6
+    caps = H.uniform_capacities(ps, 120, f_dim)
+    cfg = H.SimConfig(epochs=4, policy="jaca", staleness_bound=1, f_dim=f_dim, L=2)
+    rep = _train(g, ps, caps, cfg, kind, C, record_trace=True)
+    pr, outs, _ = oracle_run(og, ops, kind, f_dim, C, caps, "jaca", 1, 4)
+    for p in pr.plans:
+        got = [(r.local_hits, r.global_hits, r.misses) for r in rep.records if r.epoch == p.epoch]
+        assert got == [tuple(int(x) for x in c) for c in p.counts], p.epoch
+    assert rep.trace_csv == pr.trace_csv(ops.halo)
+    for e, o in enumerate(outs):
+        assert abs(rep.losses[e] - o.loss) <= TOL * abs(o.loss), e
+        assert rel_err(rep.logits_per_epoch[e], o.logits) <= TOL, e
+
+
+def test_rapa_pruned_partition_matches_oracle():
+    """A RAPA result with trimmed halos and a permuted sigma (made by the
+    reference CLI, tests/golden/cli): edges from pruned halo vertices are
+    dropped, degrees stay global (A5)."""
+    import os
+    from oracle import halo_port as ohp
+    from paper_2508_13716_b200 import artifacts as A, hostgraph as H
+    gold = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "cli")
+    g = A.load_edge_list(os.path.join(gold, "graph.txt"))
+    res, ps = A.import_rapa_result(os.path.join(gold, "rapa.json"))
+    full = H.build_partition_set(g, np.concatenate(
+        [np.full(x.size, i) for i, x in enumerate(ps.inner)])[np.argsort(np.concatenate(ps.inner))], 1)
+    assert any(a.size < b.size for a, b in zip(ps.halo, full.halo))   # really pruned
+    og = ohp.er_graph(400, 8.0, 3)
+    assert np.array_equal(og.in_tgt, g.in_targets)
+    ops = ohp.Partitions(n=g.n_vertices, P=ps.P, parts=None, inner=ps.inner, halo=ps.halo,
+                         hops=1, overlap=ps.overlap_count, cut=ps.cut_edges,
+                         all_edges=ps.all_edges)
+    f_dim, C = (16, 32), 7
+    caps = H.uniform_capacities(ps, 40, f_dim)
+    cfg = H.SimConfig(epochs=4, policy="jaca", staleness_bound=1, f_dim=f_dim, L=2)
+    from paper_2508_13716_b200 import api
+    rep = api.train(g, res, A.load_device_profiles(os.path.join(gold, "devices.json")), caps, cfg,
+                    model="gcn", num_classes=C, keep_logits="all", record_trace=True,
+                    gemm="3xtf32")
+    pr, outs, _ = oracle_run(og, ops, "gcn", f_dim, C, caps, "jaca", 1, 4)
+    assert rep.trace_csv == pr.trace_csv(ops.halo)
+    for e, o in enumerate(outs):
+        assert abs(rep.losses[e] - o.loss) <= TOL * abs(o.loss), e
+        assert rel_err(rep.logits_per_epoch[e], o.logits) <= TOL, e
