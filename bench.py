@@ -133,6 +133,17 @@ def spmm_bytes(nnz: int, rows: int, F: int, n_halo: int) -> int:
     return nnz * (4 + 4 * F) + rows * (8 + 4 + 4 * F) + 8 + n_halo * 4
 
 
+def max_over_ranks(x: float, world: int, backend: str) -> float:
+    """The slowest rank's time (every multi-GPU number is max over ranks)."""
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], device="cuda" if backend == "nccl" else "cpu", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -140,10 +151,15 @@ def run_ours(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; --dist-backend gloo exists to exercise the N > 1
+    # path with several ranks sharing one GPU (NCCL refuses that)
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.dist_backend)
     t_setup = time.perf_counter()
     g, ps, caps = build_workload(args.parts)
     cfg = H.SimConfig(epochs=args.warmup + args.steps, policy="jaca",
@@ -181,10 +197,7 @@ def run_ours(args):
     launches = _lib.launches["total"] - launches0
     sess.finish()   # completes (in place) the EpochStats of the timed epochs
     dev_ms = t0.elapsed_time(t1)
-    if world > 1:
-        t = torch.tensor([dev_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_ms = float(t.item())
+    dev_ms = max_over_ranks(dev_ms, world, args.dist_backend)
     ms_per_step = dev_ms / args.steps
     L, E = len(F_DIM), g.n_edges
     gteps = L * E * args.steps / (dev_ms / 1e3) / 1e9
@@ -247,10 +260,7 @@ def run_ours(args):
     barrier()
     w_s = time.perf_counter() - w0
     sess.finish()
-    if world > 1:
-        t = torch.tensor([w_s], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        w_s = float(t.item())
+    w_s = max_over_ranks(w_s, world, args.dist_backend)
     e2e = {"value": L * E * e2e_steps / w_s / 1e9, "unit": "GTEPS",
            "h2d_bytes_per_step": int(host_x.numel() * 4),
            "d2h_bytes_per_step": int(host_logits[0].numel() * 4 + 4),
@@ -399,6 +409,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--parts", type=int, default=PARTS)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help=argparse.SUPPRESS)
     ap.add_argument("--staleness", type=int, default=-1)
     ap.add_argument("--gemm", default="3xtf32", choices=["fp32", "3xtf32", "tf32"])
     ap.add_argument("--cpu-budget", type=float, default=20.0)

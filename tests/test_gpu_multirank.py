@@ -110,3 +110,20 @@ def test_two_ranks_match_oracle(case):
     for e, o in enumerate(outs):
         assert abs(got["losses"][e] - o.loss) <= 1e-4 * abs(o.loss), e
         assert rel_err(got["logits"][e], o.logits) <= 1e-4, e
+
+
+def test_bench_two_ranks_one_gpu():
+    """bench.py's N > 1 path (torchrun, barriers, max over ranks, one JSON line
+    from rank 0), two ranks sharing cuda:0 over gloo."""
+    import json
+    port = _free_port()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}", "bench.py", "--gpus", "2",
+           "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--dist-backend", "gloo"]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["partitions_per_gpu"] == 4
+    assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
