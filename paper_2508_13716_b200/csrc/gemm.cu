@@ -27,6 +27,8 @@ int cg_wgrad_tc(int64_t M, int K, int N, const float *A, int64_t lda, const floa
                 cudaStream_t st);
 int cg_colsum(int64_t M, int N, const float *D, int64_t ldd, float *db, float *ws, void *stream);
 int cg_reduce_chunks(int64_t n_out, int64_t n_chunks, const float *ws, float *out, cudaStream_t st);
+int cg_reduce_chunks_pair(int64_t n1, int64_t c1, const float *ws1, float *out1, int64_t n2,
+                          int64_t c2, const float *ws2, float *out2, cudaStream_t st);
 
 namespace {
 
@@ -232,14 +234,17 @@ int cg_wgrad(int64_t M, int K, int N, const float *A, int64_t lda, const float *
         launched += 1;
     }
     int64_t n_out = (int64_t)K * N;
-    int rc = cg_reduce_chunks(n_out, nch, ws, dW, st);   // 8 warps split the chunks
-    if (rc < 0) return rc;
-    launched += rc;
-    if (fuse_db) {
-        rc = cg_reduce_chunks(N, nch * 4, bws, db, st);
+    int rc;
+    if (fuse_db) {   // dW and db partials reduced by one launch
+        rc = cg_reduce_chunks_pair(n_out, nch, ws, dW, N, nch * 4, bws, db, st);
         if (rc < 0) return rc;
         launched += rc;
-    } else if (db) {
+    } else {
+        rc = cg_reduce_chunks(n_out, nch, ws, dW, st);
+        if (rc < 0) return rc;
+        launched += rc;
+    }
+    if (!fuse_db && db) {
         int rc = cg_colsum(M, N, D, ldd, db, bws, stream);
         if (rc < 0) return rc;
         launched += rc;

@@ -403,6 +403,45 @@ k_colsum_partial(int64_t M, int N, const float *__restrict__ D, int64_t ldd,
 // keeping 4 independent partial sums so the loads pipeline), then a fixed
 // combination of the partials.
 template <int NW>
+__device__ __forceinline__ void reduce_chunks_block(int64_t blk, int64_t n_out, int64_t n_chunks,
+                                                    const float *__restrict__ ws,
+                                                    float *__restrict__ out) {
+    __shared__ float part[NW][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t i = blk * 32 + lane;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    if (i < n_out) {
+        int64_t c = w;
+        for (; c + 3 * NW < n_chunks; c += 4 * NW) {
+            s0 += ws[c * n_out + i];
+            s1 += ws[(c + NW) * n_out + i];
+            s2 += ws[(c + 2 * NW) * n_out + i];
+            s3 += ws[(c + 3 * NW) * n_out + i];
+        }
+        for (; c < n_chunks; c += NW) s0 += ws[c * n_out + i];
+    }
+    part[w][lane] = (s0 + s1) + (s2 + s3);
+    __syncthreads();
+    if (w == 0 && i < n_out) {
+        float t = 0.f;
+#pragma unroll
+        for (int k = 0; k < NW; ++k) t += part[k][lane];
+        out[i] = t;
+    }
+}
+
+// Two independent chunk reductions in one launch (the weight and the bias
+// gradient partials of one cg_wgrad call): blocks [0, nb1) do the first.
+template <int NW>
+__global__ void __launch_bounds__(NW * 32)
+k_reduce_chunks_pair(int64_t nb1, int64_t n1, int64_t c1, const float *__restrict__ ws1,
+                     float *__restrict__ out1, int64_t n2, int64_t c2,
+                     const float *__restrict__ ws2, float *__restrict__ out2) {
+    if (blockIdx.x < nb1) reduce_chunks_block<NW>(blockIdx.x, n1, c1, ws1, out1);
+    else reduce_chunks_block<NW>(blockIdx.x - nb1, n2, c2, ws2, out2);
+}
+
+template <int NW>
 __global__ void __launch_bounds__(NW * 32)
 k_reduce_chunks_tree(int64_t n_out, int64_t n_chunks, const float *__restrict__ ws,
                      float *__restrict__ out) {
@@ -669,6 +708,16 @@ inline int grid_for(int64_t work, int threads, int max_blocks = 148 * 16) {
 
 // out[i] = sum_c ws[c][i] over n_chunks partial rows, fixed order (internal
 // helper shared with the weight-gradient path in gemm.cu; not in the ABI).
+int cg_reduce_chunks_pair(int64_t n1, int64_t c1, const float *ws1, float *out1, int64_t n2,
+                          int64_t c2, const float *ws2, float *out2, cudaStream_t st) {
+    const int64_t nb1 = (n1 + 31) / 32, nb2 = (n2 + 31) / 32;
+    if (nb1 + nb2 == 0) return 0;
+    k_reduce_chunks_pair<32><<<(unsigned)(nb1 + nb2), 1024, 0, st>>>(nb1, n1, c1, ws1, out1, n2,
+                                                                     c2, ws2, out2);
+    CG_CHECK_LAUNCH("k_reduce_chunks_pair");
+    return 1;
+}
+
 int cg_reduce_chunks(int64_t n_out, int64_t n_chunks, const float *ws, float *out,
                      cudaStream_t st) {
     if (n_out == 0) return 0;

@@ -5,7 +5,7 @@ import re
 import sys
 
 
-def main(path, n_timed=2, tail_epochs=2):
+def main(path, n_timed=2, tail_epochs=4):
     rows = list(csv.reader(open(path)))
     h = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
     hdr, data = rows[h], rows[h + 1:]
@@ -13,7 +13,7 @@ def main(path, n_timed=2, tail_epochs=2):
     names = [r[ki] for r in data]
     vals = [float(r[vi].replace(",", "")) for r in data]
     idx = [i for i, n in enumerate(names) if "plan_frozen" in n]
-    # timed epochs are followed by `tail_epochs` e2e epochs
+    # the timed epochs are followed by the e2e run: 2 warm-up + --steps (2) epochs
     s, e = idx[-(n_timed + tail_epochs)], idx[-tail_epochs]
     agg = collections.defaultdict(lambda: [0, 0.0])
     for n, v in zip(names[s:e], vals[s:e]):
