@@ -113,6 +113,15 @@ __global__ void k_copy_rows(int64_t n, int F, const int32_t *__restrict__ src_id
 
 // ---------------------------------------------------------------- K1 ------
 
+// Gathered feature rows: kept in L2 (evict_last), not allocated in L1.
+__device__ __forceinline__ float4 ldg_keep(const float4 *p, uint64_t pol) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+
 #ifndef SPMM_UNR1
 #define SPMM_UNR1 4   // rows in flight per lane, one float4 chunk per lane
 #endif
@@ -139,6 +148,8 @@ k_spmm(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
        const float *__restrict__ addend, int64_t ld_add, const float *__restrict__ mask,
        int64_t ld_mask, float *__restrict__ out, int64_t ldo) {
     constexpr int UNR = (NCH == 1) ? SPMM_UNR1 : SPMM_UNR2;   // rows in flight per lane
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     const int lane = threadIdx.x & (G - 1);
     const unsigned gmask = (G == 32) ? 0xffffffffu
                                      : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
@@ -155,7 +166,7 @@ k_spmm(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
         for (int c = 0; c < NCH; ++c) {
             const int ch = lane + c * G;
             if (ch < nchunk) {
-                const float4 t = __ldg(p + ch);
+                const float4 t = ldg_keep(p + ch, pol);
                 acc[c].x += t.x; acc[c].y += t.y; acc[c].z += t.z; acc[c].w += t.w;
             }
         }
@@ -193,7 +204,7 @@ k_spmm(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
 #pragma unroll
                 for (int c = 0; c < NCH; ++c) {
                     const int ch = lane + c * G;
-                    v[u][c] = ch < nchunk ? __ldg(src + ch) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    v[u][c] = ch < nchunk ? ldg_keep(src + ch, pol) : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
 #pragma unroll
