@@ -188,9 +188,12 @@ class TrainSession:
         self.planner = SequentialPlanner(cfg.policy, caps.c_cpu, caps.c_gpu, union, score,
                                          [np.asarray(h, np.int64) for h in ps.halo], ranked)
         self.planner.warm()
+        # compact HBM layout when no row is ever staged nor read from a slab
+        compact = (cfg.policy == "jaca" and cfg.staleness_bound < 0 and
+                   all(int(c) >= h.size for c, h in zip(caps.c_gpu, ps.halo)))
         self.layout = build_layout(g, [np.asarray(x, np.int64) for x in ps.inner],
                                    [np.asarray(h, np.int64) for h in ps.halo], caps.c_gpu,
-                                   world, model)
+                                   world, model, compact=compact)
         dims = [int(f) for f in cfg.f_dim] + [int(num_classes)]
         from .models import init_params
         params = init_params(model, dims, seed)

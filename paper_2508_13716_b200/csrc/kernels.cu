@@ -644,6 +644,14 @@ __device__ __forceinline__ void plan_vertex(const cg_plan_static &st, int64_t u,
             stage_src[pos] = -1;
             continue;
         }
+        if (staging_base < 0) {
+            // compact layout (no staging rows, no slabs): a plan that needs
+            // them breaks the layout's precondition -- report, never write
+            *flag = 2;
+            halo_row[pos] = -1;
+            stage_src[pos] = -1;
+            continue;
+        }
         if (oc == 0 && !cur) {  // stale local hit: read the slab in place
             halo_row[pos] = slot;
             stage_src[pos] = -1;

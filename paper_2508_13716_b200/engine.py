@@ -303,6 +303,9 @@ class Engine:
                 halo_row[pos[direct]] = orow[direct]
                 # everything else is staged into its staging row
                 stg = need & ~st_loc & ~direct & ~ver1
+                if L.compact and (st_loc.any() or stg.any()):
+                    raise RuntimeError(f"epoch {e}: the compact layout's precondition (no "
+                                       "staged or slab reads) was violated")
                 halo_row[pos[stg]] = n_in + pos[stg]
                 s_dst[pos[stg]] = n_in + pos[stg]
                 from_owner = stg & cur
@@ -410,7 +413,7 @@ class Engine:
             call("cg_plan_frozen", C.addressof(self.k6_static), e, self.staleness, self.me,
                  ptr(k["req_ver"]), ptr(k["glob_ver"]), ptr(self.halo_row), ptr(self.stage_src),
                  ptr(self.stage_row), ptr(self.stage_dst), ptr(self.gw_slot), ptr(k["counts"]),
-                 ptr(k["flag"]), self.D.n_in, self.L.n_dev,
+                 ptr(k["flag"]), -1 if self.L.compact else self.D.n_in, self.L.n_dev,
                  ptr(k["outcome"]) if self.record_outcomes else None, self.stream())
             self.wb = None
             return "gpu", None, None
@@ -585,6 +588,10 @@ class Engine:
         if stats.planner == "gpu" and not isinstance(stats.counts, np.ndarray):
             stats.counts = stats.counts.view(self.L.P, 3).cpu().numpy()
             stats.flag = int(stats.flag.item())
+            if stats.flag == 2:
+                raise RuntimeError(
+                    f"epoch {stats.epoch}: the compact layout's precondition (no staged or "
+                    "slab reads) was violated")
             if stats.flag:
                 raise RuntimeError(
                     f"epoch {stats.epoch}: frozen-membership precondition violated (an "

@@ -89,6 +89,7 @@ class RunLayout:
     owner_dev: np.ndarray | None = None
     owner_row: np.ndarray | None = None
     halo_off: np.ndarray | None = None    # flat requester offsets per partition
+    compact: bool = False                 # X_ext = [inner | snap] (no staging, no slabs)
 
 
 def _gather_rows(off: np.ndarray, tgt: np.ndarray, rows: np.ndarray):
@@ -101,7 +102,12 @@ def _gather_rows(off: np.ndarray, tgt: np.ndarray, rows: np.ndarray):
     return tgt[base + np.arange(tot)], owner
 
 
-def build_layout(g, inner, halo, c_gpu, n_dev: int, kind: str) -> RunLayout:
+def build_layout(g, inner, halo, c_gpu, n_dev: int, kind: str,
+                 compact: bool = False) -> RunLayout:
+    """compact: the plan provably never stages a row nor reads a slab slot
+    (JACA, staleness -1, every local level holds its whole halo: all reads
+    are version-0 local hits, served by the epoch-1 snapshot), so X_ext is
+    [inner | snap] only -- for C4 12 GB instead of 86 GB per GPU."""
     n = int(g.n_vertices)
     P = len(inner)
     if n_dev < 1 or P % n_dev:
@@ -132,7 +138,7 @@ def build_layout(g, inner, halo, c_gpu, n_dev: int, kind: str) -> RunLayout:
 
     # halo membership per partition for pruning checks: sorted halo arrays
     layout = RunLayout(n=n, P=P, n_dev=n_dev, part_dev=part_dev, parts_of=parts_of,
-                       row_of=row_of)
+                       row_of=row_of, compact=compact)
     for d in range(n_dev):
         plist = list(range(d * per, (d + 1) * per))
         verts = np.concatenate([inner[p] for p in plist]).astype(np.int64)
@@ -145,10 +151,10 @@ def build_layout(g, inner, halo, c_gpu, n_dev: int, kind: str) -> RunLayout:
         n_halo = o
         halo_vertex = (np.concatenate([halo[p] for p in plist]).astype(np.int64)
                        if n_halo else np.zeros(0, np.int64))
-        slab_off, o = {}, n_in + n_halo
+        slab_off, o = {}, n_in + (0 if compact else n_halo)
         for p in plist:
             slab_off[p] = o
-            o += int(c_gpu[p])
+            o += 0 if compact else int(c_gpu[p])
         n_rows = o
 
         # ---- forward CSR: in-edges of inner rows (+ self loops for GCN)
