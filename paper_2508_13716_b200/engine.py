@@ -263,6 +263,19 @@ class Engine:
         call("cg_spmm", n_rows, F, ptr(rowptr), ptr(col), n_direct, p(halo_row), ptr(X), ldx,
              p(scale), p(addend), ld_add, p(mask), ld_mask, ptr(out), ldo, self.stream())
 
+    # NVTX phase ranges for nsys / ncu --nvtx (CG_NVTX=1); one range open at a time
+    _NVTX = os.environ.get("CG_NVTX") == "1"
+
+    def _mark(self, phase):
+        if not self._NVTX:
+            return
+        if getattr(self, "_nvtx_open", False):
+            torch.cuda.nvtx.range_pop()
+            self._nvtx_open = False
+        if phase is not None:
+            torch.cuda.nvtx.range_push(f"capgnn:{phase}")
+            self._nvtx_open = True
+
     def _g(self, i: int) -> int:
         return ptr(self.grads) + 4 * int(self.poff[i])
 
@@ -445,10 +458,12 @@ class Engine:
         t0 = mk() if timers else None
         if timers:
             t0.record()
+        self._mark("plan")
         mode, hcounts, _ = self.plan(e)
         self._consume_input()
         fwd_ev, bwd_ev = [], []
         n_in = D.n_in
+        self._mark("forward")
         # ---------------- forward
         for l in range(nL):
             F, Fo = self.F[l], self.dims[l + 1]
@@ -491,11 +506,13 @@ class Engine:
             ev = torch.cuda.Event()
             ev.record(torch.cuda.current_stream(self.dev))
             self._io["fwd"] = ev
+        self._mark("loss")
         # ---------------- loss
         n_total = self.L.n
         loss_ptr = ptr(self.grads) + 4 * self.n_params
         call("cg_softmax_ce", n_in, self.C, ptr(self.logits), self.C4, ptr(self.labels),
              1.0 / n_total, ptr(self.dL), self.C4, loss_ptr, ptr(self.ce_ws), st)
+        self._mark("backward")
         # ---------------- backward
         cur = 0
         for l in range(nL - 1, -1, -1):
@@ -558,6 +575,7 @@ class Engine:
                                trans_b=1, mask=ptr(self.X[l]), ldm=F, C=ptr(nxt), ldc=F)
             if l != nL - 1:
                 cur = 1 - cur
+        self._mark("allreduce+adam")
         # ---------------- K7 + optimizer
         self.comm.allreduce_(self.grads)
         self._gw(nL - 1)
@@ -571,6 +589,7 @@ class Engine:
         if timers:
             t1 = mk()
             t1.record()
+        self._mark(None)
         stats = EpochStats(epoch=e, loss=float("nan"), counts=hcounts, seconds=0.0,
                            spmm_fwd_ms=fwd_ev, spmm_bwd_ms=bwd_ev, planner=mode,
                            events=(t0, t1) if timers else None)
