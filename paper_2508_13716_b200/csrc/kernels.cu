@@ -13,11 +13,16 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <string>
 
 #include "../../include/capgnn.h"
 
 extern void cg_set_error(const std::string &msg);
+int cg_spmm_tma(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col,
+                int64_t n_direct, const int32_t *halo_row, const float *X, int64_t ldx,
+                const float *scale, const float *addend, int64_t ld_add, const float *mask,
+                int64_t ld_mask, float *out, int64_t ldo, cudaStream_t st);
 extern int cg_cuda_fail(cudaError_t e, const char *what);
 
 #define CG_CHECK_LAUNCH(name)                                   \
@@ -799,9 +804,15 @@ int cg_spmm(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col, in
         cg_set_error("cg_spmm: F and leading dims must be multiples of 4, buffers 16-B aligned");
         return -1;
     }
+    cudaStream_t st = (cudaStream_t)stream;
+    static const bool use_tma = getenv("CG_SPMM_TMA") && atoi(getenv("CG_SPMM_TMA")) == 1;
+    if (use_tma) {   // TMA gather4 variant (spmm_tma.cu)
+        const int rc = cg_spmm_tma(n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, scale,
+                                   addend, ld_add, mask, ld_mask, out, ldo, st);
+        if (rc != 0) return rc;
+    }
     const int nchunk = F / 4;
     const int threads = 256;
-    cudaStream_t st = (cudaStream_t)stream;
 #define CG_SPMM_LAUNCH(G, NCH)                                                              \
     do {                                                                                    \
         static int blocks_per_sm = 0;                                                       \
