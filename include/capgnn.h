@@ -74,6 +74,14 @@ int cg_scale_rows_to(float *dst, int64_t ldd, const float *src, int64_t lds, int
  * dst may itself be a peer or host-tier pointer (write-through).
  * Replaces the data movement behind CacheSystem.lookup outcomes
  * (cache.py:264-309) and the "prefetch queue" of PAPER.md:98.            */
+/* Input upload (the e2e path's per-step H2D): copy n_rows x F fp32 rows from
+ * pinned, mapped host memory (`host_src`, leading dim ld_src) into device rows
+ * `dst` (leading dim ldd) with n_ctas CTAs reading over PCIe and evict-first
+ * stores; launch it on a side stream.  Replaces the copy-engine DMA so the
+ * concurrent epoch keeps its L2 working set.  F, ld_src, ldd multiples of 4. */
+int cg_upload_rows(int64_t n_rows, int F, const float *host_src, int64_t ld_src, float *dst,
+                   int64_t ldd, int n_ctas, void *stream);
+
 int cg_copy_rows(int64_t n, int F, const int32_t *src_id, const int32_t *src_row,
                  const int32_t *dst_row, const float *const *tab, const int64_t *tab_ld,
                  float *dst, int64_t ld_dst, void *stream);
@@ -137,7 +145,20 @@ int cg_softmax_ce(int64_t n_rows, int C, const float *logits, int64_t ld,
  * (as cg_split_tf32) for the pre-split 3xTF32 GEMM operands.              */
 int cg_adam(int64_t n, float *param, const float *grad, float *m, float *v,
             float lr, float beta1, float beta2, float eps, int step, float *p_hi,
-            float *p_lo, void *stream);
+            float *p_lo, const float *corr_dev, void *stream);
+
+/* ---- epoch graphs (CUDA graph replay of a steady-state epoch) ---------- *
+ * Inside a captured epoch the per-epoch scalars are read from device memory:
+ * cg_plan_frozen's epoch from `epoch_dev`, cg_adam's bias corrections
+ * (1 - beta1^t, 1 - beta2^t) from `corr_dev[2]` (each NULL = use the
+ * argument).  cg_set_epoch writes both ahead of a replay, computing the
+ * corrections exactly as cg_adam does for `step` (corr_dev may be NULL).  */
+int cg_set_epoch(int32_t *epoch_dev, int epoch, float *corr_dev, float beta1, float beta2,
+                 int step, void *stream);
+/* Record a cudaEvent_t on `stream`; while the stream is being captured the
+ * record becomes an external event node that fires on every replay (so
+ * per-kernel CUDA-event timing works inside an epoch graph).              */
+int cg_event_record(void *event, void *stream);
 
 /* ---- K6: frozen-membership JACA/FIFO plan for one epoch ---------------- *
  * One thread per halo-union vertex u; requesters of u (partition slots whose
@@ -175,7 +196,7 @@ int cg_plan_frozen(const cg_plan_static *st, int epoch, int staleness, int me,
                    int32_t *halo_row, int32_t *stage_src, int32_t *stage_row,
                    int32_t *stage_dst, int32_t *gw_slot, int64_t *counts,
                    int32_t *flag, int32_t staging_base, int32_t n_devices,
-                   int8_t *outcome, void *stream);
+                   int8_t *outcome, const int32_t *epoch_dev, void *stream);
 
 /* ---- host-side sequential two-level planner (exact CacheSystem) -------- *
  * Replaces CacheSystem (cache.py:227-382) + simulator.run's lookup loop

@@ -50,6 +50,7 @@ SIGNATURES = {
     "cg_scale_rows": [P, I64, I64, INT, P, P],
     "cg_scale_rows_to": [P, I64, P, I64, I64, INT, P, P],
     "cg_copy_rows": [I64, INT, P, P, P, P, P, P, I64, P],
+    "cg_upload_rows": [I64, INT, P, I64, P, I64, INT, P],
     "cg_spmm": [I64, INT, P, P, I64, P, P, I64, P, P, I64, P, I64, P, I64, P],
     "cg_gemm": [I64, INT, INT, P, I64, P, INT, P, I64, P, INT, P, INT, P, P, I64, P, I64, INT,
                 P, P, P],
@@ -59,8 +60,10 @@ SIGNATURES = {
     "cg_wgrad": [I64, INT, INT, P, I64, P, I64, P, P, P, INT, P],
     "cg_colsum": [I64, INT, P, I64, P, P, P],
     "cg_softmax_ce": [I64, INT, P, I64, P, F32, P, I64, P, P, P],
-    "cg_adam": [I64, P, P, P, P, F32, F32, F32, F32, INT, P, P, P],
-    "cg_plan_frozen": [P, INT, INT, INT, P, P, P, P, P, P, P, P, P, I32, I32, P, P],
+    "cg_adam": [I64, P, P, P, P, F32, F32, F32, F32, INT, P, P, P, P],
+    "cg_set_epoch": [P, INT, P, F32, F32, INT, P],
+    "cg_event_record": [P, P],
+    "cg_plan_frozen": [P, INT, INT, INT, P, P, P, P, P, P, P, P, P, I32, I32, P, P, P],
     "cg_planner_create": [INT, INT, I64, P, I64, P, P],
     "cg_planner_destroy": [P],
     "cg_planner_set_halos": [P, P, P, P],
@@ -115,10 +118,10 @@ def lib():
 # device entry points report how many kernels they launched; the running
 # total is the bench's "gpu_launches" evidence
 KERNEL_ENTRY = {"cg_hash_features", "cg_hash_labels", "cg_scale_rows", "cg_scale_rows_to",
-                "cg_copy_rows",
+                "cg_copy_rows", "cg_upload_rows",
                 "cg_spmm", "cg_gemm", "cg_wgrad", "cg_colsum", "cg_softmax_ce", "cg_adam",
                 "cg_split_tf32", "cg_split_tf32_t",
-                "cg_plan_frozen"}
+                "cg_plan_frozen", "cg_set_epoch"}
 launches = {"total": 0}
 
 
@@ -134,6 +137,13 @@ def call(name: str, *args) -> int:
         launches["total"] += rc
         launches[name] = launches.get(name, 0) + rc
     return rc
+
+
+def count_replay(per_entry: dict) -> None:
+    """A CUDA-graph replay launches the kernels its capture recorded."""
+    for name, n in per_entry.items():
+        launches["total"] += n
+        launches[name] = launches.get(name, 0) + n
 
 
 def exported_symbols() -> list[str]:

@@ -546,8 +546,10 @@ __device__ __forceinline__ void split_tf32(float x, float &hi, float &lo) {
 
 __global__ void k_adam(int64_t n, float *__restrict__ p, const float *__restrict__ g,
                        float *__restrict__ m, float *__restrict__ v, float lr, float b1,
-                       float b2, float eps, float c1, float c2, float *__restrict__ p_hi,
-                       float *__restrict__ p_lo) {
+                       float b2, float eps, float c1_arg, float c2_arg, float *__restrict__ p_hi,
+                       float *__restrict__ p_lo, const float *__restrict__ corr_dev) {
+    // bias corrections: arguments, or device-resident under graph replay
+    const float c1 = corr_dev ? corr_dev[0] : c1_arg, c2 = corr_dev ? corr_dev[1] : c2_arg;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         float gi = g[i];
@@ -691,11 +693,12 @@ __device__ __forceinline__ void plan_vertex(const cg_plan_static &st, int64_t u,
 
 constexpr int kPlanMaxParts = 256;
 __global__ void __launch_bounds__(256)
-k_plan_frozen(cg_plan_static st, int e, int s, int me, int32_t *req_ver,
+k_plan_frozen(cg_plan_static st, int e_arg, int s, int me, int32_t *req_ver,
               int32_t *glob_ver, int32_t *halo_row, int32_t *stage_src,
               int32_t *stage_row, int32_t *stage_dst, int32_t *gw_slot,
               int64_t *counts, int32_t *flag, int32_t staging_base,
-              int32_t n_devices, int8_t *outcome) {
+              int32_t n_devices, int8_t *outcome, const int32_t *epoch_dev) {
+    const int e = epoch_dev ? *epoch_dev : e_arg;   // device-resident under graph replay
     // outcome counters: shared-memory tallies, one global add per block
     __shared__ unsigned int tally[3 * kPlanMaxParts];
     for (int i = threadIdx.x; i < 3 * st.n_parts; i += blockDim.x) tally[i] = 0;
@@ -791,6 +794,53 @@ int cg_copy_rows(int64_t n, int F, const int32_t *src_id, const int32_t *src_row
         k_copy_rows<false><<<blocks, threads, 0, (cudaStream_t)stream>>>(
             n, F, src_id, src_row, dst_row, tab, tab_ld, dst, ld_dst);
     CG_CHECK_LAUNCH("k_copy_rows");
+    return 1;
+}
+
+// Input upload by the SMs: rows pulled straight out of pinned (mapped) host
+// memory over PCIe, stored with the streaming (evict-first) hint.  An
+// alternative to the copy engine for the per-step input; measured slower on
+// C2 (its CTAs hold SM slots the persistent epoch kernels wait for), so the
+// engine uses the copy engine unless CG_UPLOAD_CTAS > 0.
+__global__ void k_upload_rows(int64_t n4, int64_t f4, const float4 *__restrict__ src,
+                              int64_t ls4, float4 *__restrict__ dst, int64_t ld4) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    constexpr int U = 8;
+    for (; i + (U - 1) * stride < n4; i += U * stride) {
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t k = i + u * stride, r = k / f4, c = k - r * f4;
+            v[u] = __ldcs(src + r * ls4 + c);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t k = i + u * stride, r = k / f4, c = k - r * f4;
+            __stcs(dst + r * ld4 + c, v[u]);
+        }
+    }
+    for (; i < n4; i += stride) {
+        const int64_t r = i / f4, c = i - r * f4;
+        __stcs(dst + r * ld4 + c, __ldcs(src + r * ls4 + c));
+    }
+}
+
+int cg_upload_rows(int64_t n_rows, int F, const float *host_src, int64_t ld_src, float *dst,
+                   int64_t ldd, int n_ctas, void *stream) {
+    if (n_rows == 0 || F == 0) return 0;
+    if (F % 4 || ld_src % 4 || ldd % 4 || ((uintptr_t)host_src % 16) || ((uintptr_t)dst % 16)) {
+        cg_set_error("cg_upload_rows: F and leading dims must be multiples of 4, 16-B aligned");
+        return -1;
+    }
+    void *dsrc = nullptr;
+    cudaError_t e = cudaHostGetDevicePointer(&dsrc, const_cast<float *>(host_src), 0);
+    if (e != cudaSuccess) return cg_cuda_fail(e, "cg_upload_rows: source is not mapped pinned memory");
+    if (n_ctas <= 0) n_ctas = 16;
+    k_upload_rows<<<n_ctas, 256, 0, (cudaStream_t)stream>>>(
+        n_rows * (F / 4), F / 4, reinterpret_cast<const float4 *>(dsrc), ld_src / 4,
+        reinterpret_cast<float4 *>(dst), ldd / 4);
+    CG_CHECK_LAUNCH("k_upload_rows");
     return 1;
 }
 
@@ -901,20 +951,54 @@ int cg_softmax_ce(int64_t n_rows, int C, const float *logits, int64_t ld, const 
     return 2;
 }
 
+static void adam_corrections(float beta1, float beta2, int step, float *c1, float *c2) {
+    *c1 = (float)(1.0 - pow((double)beta1, (double)step));
+    *c2 = (float)(1.0 - pow((double)beta2, (double)step));
+}
+
 int cg_adam(int64_t n, float *param, const float *grad, float *m, float *v, float lr,
             float beta1, float beta2, float eps, int step, float *p_hi, float *p_lo,
-            void *stream) {
+            const float *corr_dev, void *stream) {
     if (n == 0) return 0;
     if ((p_hi == nullptr) != (p_lo == nullptr)) {
         cg_set_error("cg_adam: p_hi and p_lo must both be set or both be NULL");
         return -1;
     }
-    double c1 = 1.0 - pow((double)beta1, (double)step);
-    double c2 = 1.0 - pow((double)beta2, (double)step);
+    float c1, c2;
+    adam_corrections(beta1, beta2, step, &c1, &c2);
     k_adam<<<grid_for(n, 256, 148 * 8), 256, 0, (cudaStream_t)stream>>>(
-        n, param, grad, m, v, lr, beta1, beta2, eps, (float)c1, (float)c2, p_hi, p_lo);
+        n, param, grad, m, v, lr, beta1, beta2, eps, c1, c2, p_hi, p_lo, corr_dev);
     CG_CHECK_LAUNCH("k_adam");
     return 1;
+}
+
+__global__ void k_set_epoch(int32_t *epoch_dev, int epoch, float *corr_dev, float c1, float c2) {
+    *epoch_dev = epoch;
+    if (corr_dev) {
+        corr_dev[0] = c1;
+        corr_dev[1] = c2;
+    }
+}
+
+int cg_set_epoch(int32_t *epoch_dev, int epoch, float *corr_dev, float beta1, float beta2,
+                 int step, void *stream) {
+    float c1, c2;
+    adam_corrections(beta1, beta2, step, &c1, &c2);
+    k_set_epoch<<<1, 1, 0, (cudaStream_t)stream>>>(epoch_dev, epoch, corr_dev, c1, c2);
+    CG_CHECK_LAUNCH("k_set_epoch");
+    return 1;
+}
+
+int cg_event_record(void *event, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaError_t e = cudaStreamIsCapturing(st, &cs);
+    if (e != cudaSuccess) return cg_cuda_fail(e, "cudaStreamIsCapturing");
+    // under capture an external record node fires (and timestamps) on every replay
+    e = cs == cudaStreamCaptureStatusActive
+            ? cudaEventRecordWithFlags((cudaEvent_t)event, st, cudaEventRecordExternal)
+            : cudaEventRecord((cudaEvent_t)event, st);
+    return e == cudaSuccess ? 0 : cg_cuda_fail(e, "cg_event_record");
 }
 
 int cg_split_tf32_t(int n_mats, const int64_t *off, const int32_t *rows, const int32_t *cols,
@@ -936,7 +1020,8 @@ int cg_split_tf32(int64_t n, const float *x, float *hi, float *lo, void *stream)
 int cg_plan_frozen(const cg_plan_static *st, int epoch, int staleness, int me, int32_t *req_ver,
                    int32_t *glob_ver, int32_t *halo_row, int32_t *stage_src, int32_t *stage_row,
                    int32_t *stage_dst, int32_t *gw_slot, int64_t *counts, int32_t *flag,
-                   int32_t staging_base, int32_t n_devices, int8_t *outcome, void *stream) {
+                   int32_t staging_base, int32_t n_devices, int8_t *outcome,
+                   const int32_t *epoch_dev, void *stream) {
     if (st->n_union == 0) return 0;
     if (st->n_parts > kPlanMaxParts) {
         cg_set_error("cg_plan_frozen: too many partition slots");
@@ -944,7 +1029,7 @@ int cg_plan_frozen(const cg_plan_static *st, int epoch, int staleness, int me, i
     }
     k_plan_frozen<<<(unsigned)((st->n_union + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
         *st, epoch, staleness, me, req_ver, glob_ver, halo_row, stage_src, stage_row, stage_dst,
-        gw_slot, counts, flag, staging_base, n_devices, outcome);
+        gw_slot, counts, flag, staging_base, n_devices, outcome, epoch_dev);
     CG_CHECK_LAUNCH("k_plan_frozen");
     return 1;
 }

@@ -15,12 +15,15 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from . import _lib
 from ._lib import PlanStatic, call, ptr
 from .comm import HostTier, SoloComm
 from .layout import RunLayout
 from .planner import EpochPlan, SequentialPlanner
 
 GEMM_MODES = {"fp32": 0, "3xtf32": 1, "tf32": 2}
+# CTAs of the SM-driven input upload (cg_upload_rows); 0 = copy-engine DMA (default)
+_UPLOAD_CTAS = int(os.environ.get("CG_UPLOAD_CTAS", "0"))
 
 
 def _dev(a, dtype, device):
@@ -45,7 +48,8 @@ class Engine:
                  caps, planner: SequentialPlanner, staleness: int, policy: str,
                  comm=None, lr: float = 0.01, gemm: str = "fp32", params_init=None,
                  device: int | None = None, freeze_epoch: int | None = None,
-                 record_outcomes: bool = False, plan_mode: str = "auto"):
+                 record_outcomes: bool = False, plan_mode: str = "auto",
+                 graphs: bool | None = None):
         self.L = layout
         self.me = me
         self.D = layout.devices[me]
@@ -71,6 +75,13 @@ class Engine:
         self.freeze_epoch = freeze_epoch if freeze_epoch is not None else max(1, staleness + 1)
         self.gpu_plan_ready = False
         self.step = 0
+        # steady-state epochs (K6-planned, one process) replay CUDA graphs;
+        # CG_GRAPHS=0 keeps every epoch eager
+        if graphs is None:
+            graphs = os.environ.get("CG_GRAPHS", "1") != "0"
+        self.use_graphs = bool(graphs) and isinstance(self.comm, SoloComm)
+        self._capturing = False
+        self._graphs = None
         self._alloc(caps, params_init)
 
     # ------------------------------------------------------------------ setup
@@ -136,6 +147,9 @@ class Engine:
         self.grads = torch.zeros(self.n_params + 1, dtype=f32, device=dev)
         self.adam_m = torch.zeros(self.n_params, dtype=f32, device=dev)
         self.adam_v = torch.zeros(self.n_params, dtype=f32, device=dev)
+        # per-epoch scalars read by kernels inside an epoch graph (cg_set_epoch)
+        self.epoch_dev = torch.zeros(1, dtype=i32, device=dev)
+        self.adam_corr = torch.zeros(2, dtype=f32, device=dev)
         ws = 1
         for l in range(self.nL):
             ws = max(ws, call("cg_wgrad_workspace", D.n_in, dims[l], dims[l + 1]),
@@ -427,7 +441,8 @@ class Engine:
                  ptr(k["req_ver"]), ptr(k["glob_ver"]), ptr(self.halo_row), ptr(self.stage_src),
                  ptr(self.stage_row), ptr(self.stage_dst), ptr(self.gw_slot), ptr(k["counts"]),
                  ptr(k["flag"]), -1 if self.L.compact else self.D.n_in, self.L.n_dev,
-                 ptr(k["outcome"]) if self.record_outcomes else None, self.stream())
+                 ptr(k["outcome"]) if self.record_outcomes else None,
+                 ptr(self.epoch_dev) if self._capturing else None, self.stream())
             self.wb = None
             return "gpu", None, None
         if self.gpu_plan_ready:
@@ -451,20 +466,16 @@ class Engine:
                    self.tab[l], self.tab_ld[l], self.host.ptr + 4 * int(self.layer_off[l]),
                    self.bpe_f)
 
-    def run_epoch(self, e: int, timers: bool = True, sync: bool = True) -> EpochStats:
-        D, st, nL, kind = self.D, self.stream(), self.nL, self.kind
-        ev = []
-        mk = (lambda: torch.cuda.Event(enable_timing=True)) if timers else None
-        t0 = mk() if timers else None
-        if timers:
-            t0.record()
-        self._mark("plan")
-        mode, hcounts, _ = self.plan(e)
-        self._consume_input()
-        fwd_ev, bwd_ev = [], []
-        n_in = D.n_in
-        self._mark("forward")
-        # ---------------- forward
+    def _rec(self, ev) -> None:
+        """Record a timing event on the current stream; inside a capture it
+        becomes an external event node that fires on every replay."""
+        if self._capturing:
+            call("cg_event_record", ev.cuda_event, self.stream())
+        else:
+            ev.record()
+
+    def _forward(self, e: int, spmm_ev) -> None:
+        D, nL, kind, n_in = self.D, self.nL, self.kind, self.D.n_in
         for l in range(nL):
             F, Fo = self.F[l], self.dims[l + 1]
             if l > 0:
@@ -477,23 +488,19 @@ class Engine:
             if D.n_halo:
                 self._copy(D.n_halo, F, self.stage_src, self.stage_row, self.stage_dst,
                            self.tab[l], self.tab_ld[l], self.X[l], F)
-            if timers:
-                a, b = mk(), mk()
-                a.record()
+            if spmm_ev is not None:
+                self._rec(spmm_ev[l][0])
             self._spmm(n_in, F, self.fwd_rowptr, self.fwd_col, n_in, self.halo_row, self.X[l],
                        F, self.norm_dst, None, 0, None, 0, self.Z[l], F)
-            if timers:
-                b.record()
-                fwd_ev.append((a, b))
+            if spmm_ev is not None:
+                self._rec(spmm_ev[l][1])
             if self.wb is not None:
                 sid, srow, dst, n = self.wb
                 self._copy(n, F, sid, srow, dst, self.tab[l], self.tab_ld[l], self.X[l], F)
             last = l == nL - 1
             out = self.logits if last else self.X[l + 1]
-            if last and self._io is not None and self._io["logits_done"] is not None:
-                # the previous epoch's logits download must finish first
-                torch.cuda.current_stream(self.dev).wait_event(self._io["logits_done"])
-                self._io["logits_done"] = None
+            if last and not self._capturing:
+                self._wait_logits_download()
             if kind == "gcn":
                 self._gemm(n_in, Fo, F, ptr(self.Z[l]), F, 2 * l, trans_b=0,
                            bias=self._p(2 * l + 1), relu=0 if last else 1,
@@ -502,18 +509,20 @@ class Engine:
                 self._gemm(n_in, Fo, F, ptr(self.X[l]), F, 3 * l, F, ptr(self.Z[l]), F,
                            3 * l + 1, trans_b=0, bias=self._p(3 * l + 2),
                            relu=0 if last else 1, C=ptr(out), ldc=Fo)
-        if self._io is not None:
-            ev = torch.cuda.Event()
-            ev.record(torch.cuda.current_stream(self.dev))
-            self._io["fwd"] = ev
-        self._mark("loss")
-        # ---------------- loss
-        n_total = self.L.n
+
+    def _wait_logits_download(self) -> None:
+        # the previous epoch's logits download must finish before they change
+        if self._io is not None and self._io["logits_done"] is not None:
+            torch.cuda.current_stream(self.dev).wait_event(self._io["logits_done"])
+            self._io["logits_done"] = None
+
+    def _loss(self) -> None:
         loss_ptr = ptr(self.grads) + 4 * self.n_params
-        call("cg_softmax_ce", n_in, self.C, ptr(self.logits), self.C4, ptr(self.labels),
-             1.0 / n_total, ptr(self.dL), self.C4, loss_ptr, ptr(self.ce_ws), st)
-        self._mark("backward")
-        # ---------------- backward
+        call("cg_softmax_ce", self.D.n_in, self.C, ptr(self.logits), self.C4, ptr(self.labels),
+             1.0 / self.L.n, ptr(self.dL), self.C4, loss_ptr, ptr(self.ce_ws), self.stream())
+
+    def _backward(self, spmm_ev) -> None:
+        st, nL, kind, n_in = self.stream(), self.nL, self.kind, self.D.n_in
         cur = 0
         for l in range(nL - 1, -1, -1):
             F, Fo = self.F[l], self.dims[l + 1]
@@ -552,9 +561,9 @@ class Engine:
             if self.n_bwd:
                 self._copy(self.n_bwd, Fx, self.b_src, self.b_row, self.b_dst, self.tabGs[l & 1],
                            self._tabG_ld(Fx), G, Fx)
-            if timers:
-                a, b = mk(), mk()
-                a.record()
+            k = nL - 1 - l
+            if spmm_ev is not None:
+                self._rec(spmm_ev[k][0])
             if wide:
                 # T = (a | 1) * A^T G, then dY_{l-1} = mask * (T W^T [+ dY W_self^T])
                 self._spmm(n_in, Fx, self.bwd_rowptr, self.bwd_col, 1 << 62, None, G, Fx,
@@ -563,9 +572,8 @@ class Engine:
                 self._spmm(n_in, F, self.bwd_rowptr, self.bwd_col, 1 << 62, None, G, F,
                            self.norm_src if kind == "gcn" else None,
                            self.Hs if kind == "sage" else None, F, self.X[l], F, nxt, F)
-            if timers:
-                b.record()
-                bwd_ev.append((a, b))
+            if spmm_ev is not None:
+                self._rec(spmm_ev[k][1])
             if wide:
                 if kind == "gcn":
                     self._gemm(n_in, F, Fo, ptr(self.T), Fo, W, trans_b=1, mask=ptr(self.X[l]),
@@ -575,23 +583,129 @@ class Engine:
                                trans_b=1, mask=ptr(self.X[l]), ldm=F, C=ptr(nxt), ldc=F)
             if l != nL - 1:
                 cur = 1 - cur
-        self._mark("allreduce+adam")
-        # ---------------- K7 + optimizer
+
+    def _update(self) -> None:
+        """K7 + optimizer + the weights' TF32 split; uses self.step."""
         self.comm.allreduce_(self.grads)
-        self._gw(nL - 1)
-        self.step += 1
+        self._gw(self.nL - 1)
         call("cg_adam", self.n_params, ptr(self.params), ptr(self.grads), ptr(self.adam_m),
              ptr(self.adam_v), self.lr, 0.9, 0.999, 1e-8, self.step,
              ptr(self.params_hi) if self.params_hi is not None else None,
-             ptr(self.params_lo) if self.params_lo is not None else None, st)
+             ptr(self.params_lo) if self.params_lo is not None else None,
+             ptr(self.adam_corr) if self._capturing else None, self.stream())
         if self.params_hi is not None:
             self._split_t()
+
+    def _new_timers(self, n: int):
+        return [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in range(n)]
+
+    # ----------------------------------------------------------- epoch graphs
+    def _graph_epoch_ok(self, e: int) -> bool:
+        """A steady-state epoch: K6-planned, no epoch-1 snapshot, one process."""
+        return (self.use_graphs and e > 1 and self.plan_mode != "host"
+                and self.policy in ("jaca", "fifo") and e > self.freeze_epoch
+                and self.L.union is not None and self.L.union.size > 0
+                and (self.gpu_plan_ready or self.planner.state()["admissions"] == 0))
+
+    def _capture(self, e: int) -> None:
+        """Capture the steady-state epoch as two CUDA graphs: plan + forward +
+        loss, then backward + K7 + optimizer (the logits-ready event for the
+        host download is recorded between the two replays).  The per-epoch
+        scalars come from epoch_dev / adam_corr, so one capture serves every
+        later epoch.  SpMM timing events are external event nodes."""
+        if not self.gpu_plan_ready:
+            self._init_gpu_plan()
+        fwd_ev, bwd_ev = self._new_timers(self.nL), self._new_timers(self.nL - 1)
+        for a, b in fwd_ev + bwd_ev:   # materialise the events before capture
+            a.record()
+            b.record()
+        self._io_state()      # copy streams exist before capture
+        pool = torch.cuda.graph_pool_handle()
+        g1, g2 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        # launches recorded by the capture run on each replay, not now
+        before = dict(_lib.launches)
+        self._capturing = True
+        try:
+            with torch.cuda.graph(g1, pool=pool):
+                self.plan(e)
+                self._forward(e, fwd_ev)
+                self._loss()
+            with torch.cuda.graph(g2, pool=pool):
+                self._backward(bwd_ev)
+                self._update()
+        finally:
+            self._capturing = False
+        recorded = {k: v - before.get(k, 0) for k, v in _lib.launches.items()
+                    if v != before.get(k, 0)}
+        _lib.count_replay({k: -v for k, v in recorded.items()})
+        self._graphs = (g1, g2, fwd_ev, bwd_ev, recorded)
+
+    def _run_epoch_graph(self, e: int, timers: bool, sync: bool) -> EpochStats:
+        if self._graphs is None:
+            self._capture(e)
+        g1, g2, fwd_ev, bwd_ev, recorded = self._graphs
+        cs = torch.cuda.current_stream(self.dev)
+        t0 = t1 = None
         if timers:
-            t1 = mk()
+            t0 = torch.cuda.Event(enable_timing=True)
+            t0.record()
+        self.step += 1
+        call("cg_set_epoch", ptr(self.epoch_dev), e, ptr(self.adam_corr), 0.9, 0.999, self.step,
+             self.stream())
+        self._consume_input()
+        self._wait_logits_download()
+        g1.replay()
+        if self._io is not None:
+            ev = torch.cuda.Event()
+            ev.record(cs)
+            self._io["fwd"] = ev
+        g2.replay()
+        _lib.count_replay(recorded)
+        if timers:
+            t1 = torch.cuda.Event(enable_timing=True)
+            t1.record()
+        # the graphs' SpMM events carry the most recent replay's times
+        stats = EpochStats(epoch=e, loss=float("nan"), counts=None, seconds=0.0,
+                           spmm_fwd_ms=list(fwd_ev) if timers else [],
+                           spmm_bwd_ms=list(bwd_ev) if timers else [], planner="gpu",
+                           events=(t0, t1) if timers else None)
+        stats.counts = self.k6["counts"].clone()
+        stats.flag = self.k6["flag"].clone()
+        stats.loss = self.grads[self.n_params:].clone()
+        return self.finish(stats) if sync else stats
+
+    def run_epoch(self, e: int, timers: bool = True, sync: bool = True) -> EpochStats:
+        if self._graph_epoch_ok(e):
+            return self._run_epoch_graph(e, timers, sync)
+        t0 = t1 = None
+        if timers:
+            t0 = torch.cuda.Event(enable_timing=True)
+            t0.record()
+        fwd_ev = self._new_timers(self.nL) if timers else None
+        bwd_ev = self._new_timers(self.nL - 1) if timers else None
+        self._mark("plan")
+        mode, hcounts, _ = self.plan(e)
+        self._consume_input()
+        self._mark("forward")
+        self._forward(e, fwd_ev)
+        if self._io is not None:
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(self.dev))
+            self._io["fwd"] = ev
+        self._mark("loss")
+        self._loss()
+        self._mark("backward")
+        self._backward(bwd_ev)
+        self._mark("allreduce+adam")
+        self.step += 1
+        self._update()
+        if timers:
+            t1 = torch.cuda.Event(enable_timing=True)
             t1.record()
         self._mark(None)
         stats = EpochStats(epoch=e, loss=float("nan"), counts=hcounts, seconds=0.0,
-                           spmm_fwd_ms=fwd_ev, spmm_bwd_ms=bwd_ev, planner=mode,
+                           spmm_fwd_ms=fwd_ev or [], spmm_bwd_ms=bwd_ev or [], planner=mode,
                            events=(t0, t1) if timers else None)
         if mode == "gpu":
             # keep this epoch's counters on the device until finish()
@@ -644,8 +758,16 @@ class Engine:
         st = io["h2d"]
         if io["free"] is not None:
             st.wait_event(io["free"])      # the previous upload has been consumed
-        with torch.cuda.stream(st):
-            io["stage"].copy_(host_x, non_blocking=True)
+        if _UPLOAD_CTAS > 0 and host_x.is_pinned() and host_x.is_contiguous():
+            # SM-driven zero-copy read (cg_upload_rows; CG_UPLOAD_CTAS > 0): an
+            # alternative measured slower -- its CTAs hold SMs the persistent
+            # epoch kernels need
+            call("cg_upload_rows", host_x.shape[0], host_x.shape[1], host_x.data_ptr(),
+                 host_x.shape[1], ptr(io["stage"]), io["stage"].shape[1], _UPLOAD_CTAS,
+                 st.cuda_stream)
+        else:
+            with torch.cuda.stream(st):
+                io["stage"].copy_(host_x, non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(st)
         io["ready"] = ev

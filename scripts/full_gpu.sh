@@ -1,0 +1,4 @@
+set -u
+OUT=gpurun_out/${1:-fx}; mkdir -p $OUT
+timeout 1500 python -m pytest tests -m gpu -q > $OUT/pytest_all.log 2>&1; echo "rc=$?" >> $OUT/pytest_all.log
+timeout 300 python bench.py --no-cpu-baseline --steps 20 > $OUT/bench.json 2>> $OUT/bench.err

@@ -87,6 +87,23 @@ def test_copy_rows_table():
     assert np.array_equal(dst.cpu().numpy(), exp)
 
 
+@pytest.mark.parametrize("n,F,lds,ldd,ctas", [(169343, 128, 128, 128, 16), (1001, 36, 40, 44, 3),
+                                              (5, 4, 4, 8, 64)])
+def test_upload_rows_from_pinned_host(n, F, lds, ldd, ctas):
+    """cg_upload_rows: SM-driven copy out of pinned host memory, bit-exact,
+    strided on both sides, rows beyond n untouched."""
+    import torch
+    from paper_2508_13716_b200._lib import call, ptr
+    host = torch.from_numpy(np.random.default_rng(n).standard_normal((n, lds)).astype(np.float32))
+    host = host.pin_memory()
+    dst = torch.full((n + 3, ldd), 7.0, device="cuda")
+    call("cg_upload_rows", n, F, host.data_ptr(), lds, ptr(dst), ldd, ctas, _st())
+    _sync()
+    got = dst.cpu().numpy()
+    assert np.array_equal(got[:n, :F], host.numpy()[:, :F])
+    assert (got[:n, F:] == 7.0).all() and (got[n:] == 7.0).all()
+
+
 @pytest.mark.parametrize("shape", [(1000, 40, 256, 0), (777, 256, 128, 0), (513, 64, 36, 1),
                                    (2048, 256, 256, 1)])
 def test_gemm_epilogue(shape):
@@ -169,8 +186,19 @@ def test_softmax_ce_and_adam(Cc, ld):
         grad = rng.standard_normal(1000).astype(np.float32)
         tg = _t(grad)
         hi, lo = torch.empty(1000, device="cuda"), torch.empty(1000, device="cuda")
+        corr = None
+        if t == 2:   # the graph-replay form: step scalars read from device memory
+            ep, corr = torch.zeros(1, dtype=torch.int32, device="cuda"), torch.zeros(2, device="cuda")
+            call("cg_set_epoch", ptr(ep), 7, ptr(corr), 0.9, 0.999, t, _st())
+            _sync()
+            assert int(ep.item()) == 7
+            # as cg_adam: 1 - beta^t in double from the float betas, rounded to float
+            b1, b2 = float(np.float32(0.9)), float(np.float32(0.999))
+            assert corr.cpu().numpy().tolist() == [float(np.float32(1 - b1 ** 2)),
+                                                    float(np.float32(1 - b2 ** 2))]
         call("cg_adam", 1000, ptr(tp), ptr(tg), ptr(tm_), ptr(tv), 0.01, 0.9, 0.999, 1e-8,
-             t, ptr(hi), ptr(lo), _st())
+             99 if corr is not None else t, ptr(hi), ptr(lo),
+             None if corr is None else ptr(corr), _st())
         _sync()
         # the emitted split: hi, lo are TF32 values, |param - hi - lo| <= 2^-23 |param|
         _check_tf32_split(tp.cpu().numpy(), hi.cpu().numpy(), lo.cpu().numpy())
