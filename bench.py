@@ -303,7 +303,16 @@ def run_ours(args):
                          "kernel": "k_spmm (fused cache-lookup + gather SpMM), all fwd+bwd "
                                    "launches of the timed epochs",
                          "bytes_per_epoch": sum(fb) + sum(bb),
-                         "spmm_ms_per_epoch": tot_ms / args.steps},
+                         "spmm_ms_per_epoch": tot_ms / args.steps,
+                         "launches": [{"pass": ps_, "F": int(w), "bytes": int(b_),
+                                       "ms": round(float(m), 4),
+                                       "GB_s": round(b_ / (float(m) / 1e3) / 1e9, 1)}
+                                      for ps_, w, b_, m in zip(
+                                          ["fwd"] * len(fb) + ["bwd"] * len(bb),
+                                          list(F_DIM) + [min(widths[l], widths[l + 1])
+                                                         for l in range(len(F_DIM) - 1, 0, -1)],
+                                          fb + bb,
+                                          list(fwd_ms.mean(0)) + list(bwd_ms.mean(0)))]},
             "halo_bytes_per_epoch": {"model_fwd_cached": fwd_model,
                                      "model_fwd_uncached": fwd_uncached,
                                      "model_bwd": bwd_model},

@@ -92,11 +92,15 @@ int cg_copy_rows(int64_t n, int F, const int32_t *src_id, const int32_t *src_row
  * epi: (+ addend[r]) then (* (mask[r] > 0)) when the pointers are non-NULL.
  * Sum order is CSR order (deterministic).  Used for the forward
  * aggregation (CSR of in-edges) and the backward (CSR of out-edges).
+ * nnz = rowptr[n_rows] - rowptr[0] when the caller knows it, else -1: it
+ * only picks the kernel (rows averaging < 64 edges with 128 < F <= 640 take
+ * the cp.async shared-memory ring kernel; results are identical either way).
  * Stand-in replaced: comp_cost's SpMM term (devices.py:119-132).         */
 int cg_spmm(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col,
             int64_t n_direct, const int32_t *halo_row, const float *X, int64_t ldx,
             const float *scale, const float *addend, int64_t ld_add,
-            const float *mask, int64_t ld_mask, float *out, int64_t ldo, void *stream);
+            const float *mask, int64_t ld_mask, float *out, int64_t ldo, int64_t nnz,
+            void *stream);
 
 /* ---- K5: dense transform ---------------------------------------------- */
 /* C[m, n] = epi( sum_k A1[m,k] B1[k,n] + sum_k A2[m,k] B2[k,n] )  (A2 optional)

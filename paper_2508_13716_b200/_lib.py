@@ -51,7 +51,7 @@ SIGNATURES = {
     "cg_scale_rows_to": [P, I64, P, I64, I64, INT, P, P],
     "cg_copy_rows": [I64, INT, P, P, P, P, P, P, I64, P],
     "cg_upload_rows": [I64, INT, P, I64, P, I64, INT, P],
-    "cg_spmm": [I64, INT, P, P, I64, P, P, I64, P, P, I64, P, I64, P, I64, P],
+    "cg_spmm": [I64, INT, P, P, I64, P, P, I64, P, P, I64, P, I64, P, I64, I64, P],
     "cg_gemm": [I64, INT, INT, P, I64, P, INT, P, I64, P, INT, P, INT, P, P, I64, P, I64, INT,
                 P, P, P],
     "cg_split_tf32": [I64, P, P, P, P],

@@ -23,6 +23,10 @@ int cg_spmm_tma(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col
                 int64_t n_direct, const int32_t *halo_row, const float *X, int64_t ldx,
                 const float *scale, const float *addend, int64_t ld_add, const float *mask,
                 int64_t ld_mask, float *out, int64_t ldo, cudaStream_t st);
+int cg_spmm_async(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col,
+                  int64_t n_direct, const int32_t *halo_row, const float *X, int64_t ldx,
+                  const float *scale, const float *addend, int64_t ld_add, const float *mask,
+                  int64_t ld_mask, float *out, int64_t ldo, cudaStream_t st);
 extern int cg_cuda_fail(cudaError_t e, const char *what);
 
 #define CG_CHECK_LAUNCH(name)                                   \
@@ -234,10 +238,14 @@ k_spmm(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
         for (int c = 0; c < NCH; ++c) {
             const int ch = lane + c * G;
             if (ch >= nchunk) continue;
-            float4 o = make_float4(acc[c].x * sc, acc[c].y * sc, acc[c].z * sc, acc[c].w * sc);
+            // explicit roundings (no FMA contraction): every SpMM kernel's epilogue
+            // rounds the same way, so they agree bit for bit
+            float4 o = make_float4(__fmul_rn(acc[c].x, sc), __fmul_rn(acc[c].y, sc),
+                                   __fmul_rn(acc[c].z, sc), __fmul_rn(acc[c].w, sc));
             if (addend) {
                 const float4 a = reinterpret_cast<const float4 *>(addend + r * ld_add)[ch];
-                o.x += a.x; o.y += a.y; o.z += a.z; o.w += a.w;
+                o.x = __fadd_rn(o.x, a.x); o.y = __fadd_rn(o.y, a.y);
+                o.z = __fadd_rn(o.z, a.z); o.w = __fadd_rn(o.w, a.w);
             }
             if (mask) {
                 const float4 m = reinterpret_cast<const float4 *>(mask + r * ld_mask)[ch];
@@ -847,7 +855,7 @@ int cg_upload_rows(int64_t n_rows, int F, const float *host_src, int64_t ld_src,
 int cg_spmm(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col, int64_t n_direct,
             const int32_t *halo_row, const float *X, int64_t ldx, const float *scale,
             const float *addend, int64_t ld_add, const float *mask, int64_t ld_mask, float *out,
-            int64_t ldo, void *stream) {
+            int64_t ldo, int64_t nnz, void *stream) {
     if (n_rows == 0) return 0;
     if (F % 4 || ldx % 4 || ldo % 4 || (addend && ld_add % 4) || (mask && ld_mask % 4) ||
         ((uintptr_t)X % 16) || ((uintptr_t)out % 16)) {
@@ -855,6 +863,18 @@ int cg_spmm(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col, in
         return -1;
     }
     cudaStream_t st = (cudaStream_t)stream;
+    // 128 < F <= 640 with sparse rows: the cp.async shared-memory ring kernel
+    // (spmm_async.cu).  Measured: C2 (8 edges/row) 0.21 vs 0.25-0.29 ms and C4
+    // (25/row) 11.0 vs 11.6 ms per 256-wide launch; C3 (490/row, gathers
+    // mostly L2 hits) 14.1 vs 8.2 ms, so dense rows stay on the register-
+    // pipelined kernel below.  CG_SPMM_ASYNC=0 / 1 forces either choice.
+    static const int async_env = getenv("CG_SPMM_ASYNC") ? atoi(getenv("CG_SPMM_ASYNC")) : -1;
+    const bool use_async = async_env == 1 || (async_env != 0 && nnz >= 0 && nnz < 64 * n_rows);
+    if (use_async) {
+        const int rc = cg_spmm_async(n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, scale,
+                                     addend, ld_add, mask, ld_mask, out, ldo, st);
+        if (rc != 0) return rc;
+    }
     static const bool use_tma = getenv("CG_SPMM_TMA") && atoi(getenv("CG_SPMM_TMA")) == 1;
     if (use_tma) {   // TMA gather4 variant (spmm_tma.cu)
         const int rc = cg_spmm_tma(n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, scale,

@@ -168,10 +168,13 @@ k_spmm_g4(const __grid_constant__ CUtensorMap mX, int64_t n_rows, int F,
         for (int c = 0; c < NCH; ++c) {
             const int ch = lane + 32 * c;
             if (ch >= nchunk) continue;
-            float4 o = make_float4(acc[c].x * srow, acc[c].y * srow, acc[c].z * srow,
-                                   acc[c].w * srow);
+            // explicit roundings (no FMA contraction): every SpMM kernel's epilogue
+            // rounds the same way, so they agree bit for bit
+            float4 o = make_float4(__fmul_rn(acc[c].x, srow), __fmul_rn(acc[c].y, srow),
+                                   __fmul_rn(acc[c].z, srow), __fmul_rn(acc[c].w, srow));
             if (addend) {
-                o.x += pa[c].x; o.y += pa[c].y; o.z += pa[c].z; o.w += pa[c].w;
+                o.x = __fadd_rn(o.x, pa[c].x); o.y = __fadd_rn(o.y, pa[c].y);
+                o.z = __fadd_rn(o.z, pa[c].z); o.w = __fadd_rn(o.w, pa[c].w);
             }
             if (mask) {
                 o.x = pm[c].x > 0.f ? o.x : 0.f; o.y = pm[c].y > 0.f ? o.y : 0.f;

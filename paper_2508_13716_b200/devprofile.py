@@ -76,7 +76,8 @@ def measure(device: int = 0, n: int = 16384, reps: int = 50, density: float = 0.
     def spmm():
         for c0 in range(0, n, W):
             call("cg_spmm", n, min(W, n - c0), ptr(t_rp), ptr(t_col), 1 << 62, None,
-                 ptr(B) + 4 * c0, n, None, None, 0, None, 0, ptr(C) + 4 * c0, n, st())
+                 ptr(B) + 4 * c0, n, None, None, 0, None, 0, ptr(C) + 4 * c0, n, cols.size,
+                 st())
 
     spmm_s = _timed(spmm, reps)
 

@@ -274,8 +274,10 @@ class Engine:
         column slices was measured slower on C2: per-row index work grows
         with the slice count faster than the L2 hit rate pays back.)"""
         p = lambda t: None if t is None else ptr(t)  # noqa: E731
+        nnz = self.D.nnz_fwd if rowptr is self.fwd_rowptr else self.D.nnz_bwd
         call("cg_spmm", n_rows, F, ptr(rowptr), ptr(col), n_direct, p(halo_row), ptr(X), ldx,
-             p(scale), p(addend), ld_add, p(mask), ld_mask, ptr(out), ldo, self.stream())
+             p(scale), p(addend), ld_add, p(mask), ld_mask, ptr(out), ldo, int(nnz),
+             self.stream())
 
     # NVTX phase ranges for nsys / ncu --nvtx (CG_NVTX=1); one range open at a time
     _NVTX = os.environ.get("CG_NVTX") == "1"

@@ -33,7 +33,7 @@ def _sync():
     torch.cuda.synchronize()
 
 
-@pytest.mark.parametrize("F", [4, 32, 64, 100, 128, 256, 604])
+@pytest.mark.parametrize("F", [4, 32, 64, 100, 128, 132, 256, 384, 500, 604])
 def test_spmm_with_halo_indirection(F):
     import torch
     from paper_2508_13716_b200._lib import call, ptr
@@ -55,11 +55,17 @@ def test_spmm_with_halo_indirection(F):
     ref = np.where(mask > 0, ref, 0.0)
     tX, tr, tc, th = _t(X), _t(rowptr), _t(col), _t(halo_row)
     ts, ta, tm = _t(scale), _t(add), _t(mask)
-    out = torch.zeros(n_rows, F, device="cuda")
-    call("cg_spmm", n_rows, F, ptr(tr), ptr(tc), n_direct, ptr(th), ptr(tX), F, ptr(ts), ptr(ta),
-         F, ptr(tm), F, ptr(out), F, _st())
-    _sync()
-    np.testing.assert_allclose(out.cpu().numpy(), ref, rtol=1e-5, atol=1e-4)
+    outs = []
+    # nnz = -1: the register-pipelined kernel; the true nnz (avg 20 edges/row)
+    # selects the cp.async ring kernel for 128 < F <= 640.  Both in CSR order.
+    for nnz in (-1, int(rowptr[-1])):
+        out = torch.zeros(n_rows, F, device="cuda")
+        call("cg_spmm", n_rows, F, ptr(tr), ptr(tc), n_direct, ptr(th), ptr(tX), F, ptr(ts),
+             ptr(ta), F, ptr(tm), F, ptr(out), F, nnz, _st())
+        _sync()
+        np.testing.assert_allclose(out.cpu().numpy(), ref, rtol=1e-5, atol=1e-4)
+        outs.append(out)
+    assert torch.equal(outs[0], outs[1])
 
 
 def test_copy_rows_table():
