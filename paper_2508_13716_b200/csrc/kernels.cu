@@ -863,13 +863,20 @@ int cg_spmm(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col, in
         return -1;
     }
     cudaStream_t st = (cudaStream_t)stream;
-    // 128 < F <= 640 with sparse rows: the cp.async shared-memory ring kernel
-    // (spmm_async.cu).  Measured: C2 (8 edges/row) 0.21 vs 0.25-0.29 ms and C4
-    // (25/row) 11.0 vs 11.6 ms per 256-wide launch; C3 (490/row, gathers
-    // mostly L2 hits) 14.1 vs 8.2 ms, so dense rows stay on the register-
-    // pipelined kernel below.  CG_SPMM_ASYNC=0 / 1 forces either choice.
+    // Sparse rows (< 64 edges on average): the cp.async shared-memory ring
+    // kernel (spmm_async.cu) for F > 128, and for 64 < F <= 128 when the
+    // gathered rows fit in L2 (estimated as n_rows x F x 4 <= 96 MB).
+    // Measured: C2 (8 edges/row) 256-wide 0.21 vs 0.25-0.29 ms, 128-wide (L2-
+    // resident) 0.096 vs 0.128 ms, 40-wide 0.068 vs 0.061 ms; C4 (25/row)
+    // 256-wide 11.0 vs 11.6 ms but 100-wide (HBM-bound) 6.2 vs 5.6 ms; C3
+    // (490/row, gathers mostly L2 hits) 256-wide 14.1 vs 8.2 ms.  Everything
+    // else stays on the register-pipelined kernel below.  CG_SPMM_ASYNC=0 / 1
+    // forces either choice.
     static const int async_env = getenv("CG_SPMM_ASYNC") ? atoi(getenv("CG_SPMM_ASYNC")) : -1;
-    const bool use_async = async_env == 1 || (async_env != 0 && nnz >= 0 && nnz < 64 * n_rows);
+    const bool sparse = nnz >= 0 && nnz < 64 * n_rows;
+    const bool fits_l2 = n_rows * (int64_t)F * 4 <= (int64_t)96 << 20;
+    const bool use_async =
+        async_env == 1 || (async_env != 0 && sparse && (F > 128 || (F > 64 && fits_l2)));
     if (use_async) {
         const int rc = cg_spmm_async(n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, scale,
                                      addend, ld_add, mask, ld_mask, out, ldo, st);

@@ -37,9 +37,10 @@ __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// NCH float4 chunks per lane (F <= 128 NCH), S ring slots per warp, EPI: an
-// addend and/or mask operand is present (its prefetch registers otherwise vanish)
-template <int NCH, int S, bool EPI>
+// G lanes per edge stream (a warp runs 32/G independent streams), NCH float4
+// chunks per lane (F <= 4 G NCH), S ring slots per stream, EPI: an addend
+// and/or mask operand is present (its prefetch registers otherwise vanish)
+template <int G, int NCH, int S, bool EPI>
 __global__ void __launch_bounds__(WARPS * 32)
 k_spmm_cpa(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
            const int32_t *__restrict__ col, int64_t n_direct, const int32_t *__restrict__ halo_row,
@@ -47,15 +48,17 @@ k_spmm_cpa(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
            const float *__restrict__ addend, int64_t ld_add, const float *__restrict__ mask,
            int64_t ld_mask, float *__restrict__ out, int64_t ldo, int64_t rows_per_warp) {
     extern __shared__ __align__(16) float4 ring_all[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float4 *ring = ring_all + (size_t)warp * S * NCH * 32;   // [slot][chunk][lane]
+    const int grp = threadIdx.x / G, lane = threadIdx.x & (G - 1);
+    const unsigned gmask = G == 32 ? 0xffffffffu
+                                   : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+    float4 *ring = ring_all + (size_t)grp * S * NCH * G;   // [slot][chunk][lane]
     const uint32_t ring_s = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
 
     // rows fit int32 (n_rows < 2^31); edge offsets are relative to the warp's
     // first edge (a warp's slice is far below 2^31 edges)
-    const int64_t gw = (int64_t)blockIdx.x * WARPS + warp;
+    const int64_t gw = (int64_t)blockIdx.x * (WARPS * 32 / G) + grp;
     if (gw * rows_per_warp >= n_rows) return;
     const int32_t r_begin = (int32_t)(gw * rows_per_warp);
     const int32_t r_end = (int32_t)(r_begin + rows_per_warp < n_rows ? r_begin + rows_per_warp
@@ -74,26 +77,26 @@ k_spmm_cpa(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
     auto raw_at = [&](int32_t i) -> int32_t { return i < n_edges ? colw[i] : 0; };
     int32_t win = 0;
     int32_t cur = resolve(raw_at(lane));
-    int32_t nxt = resolve(raw_at(32 + lane));
-    int32_t raw = raw_at(64 + lane);
+    int32_t nxt = resolve(raw_at(G + lane));
+    int32_t raw = raw_at(2 * G + lane);
 
     int32_t issued = 0;   // next edge to copy
     int s_iss = 0;        // its ring slot (issued % S)
     auto issue_one = [&]() {
         if (issued < n_edges) {
-            if (issued >= win + 32) {
-                win += 32;
+            if (issued >= win + G) {
+                win += G;
                 cur = nxt;
                 nxt = resolve(raw);
-                raw = raw_at(win + 64 + lane);
+                raw = raw_at(win + 2 * G + lane);
             }
-            const int32_t src = __shfl_sync(0xffffffffu, cur, issued - win);
+            const int32_t src = __shfl_sync(gmask, cur, issued - win, G);
             const float4 *p = reinterpret_cast<const float4 *>(X + (int64_t)src * ldx);
 #pragma unroll
             for (int c = 0; c < NCH; ++c) {
-                const int ch = lane + 32 * c;
+                const int ch = lane + G * c;
                 if (ch < nchunk)
-                    cp_async16(ring_s + (uint32_t)(((s_iss * NCH + c) * 32 + lane) * 16), p + ch,
+                    cp_async16(ring_s + (uint32_t)(((s_iss * NCH + c) * G + lane) * 16), p + ch,
                                pol);
             }
         }
@@ -108,9 +111,9 @@ k_spmm_cpa(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
         return r < r_end ? (int32_t)(rowptr[r + 1] - E0) : n_edges + 1;
     };
     auto sc_at = [&](int32_t r) -> float { return (scale && r < r_end) ? scale[r] : 1.f; };
-    int32_t rp = rp_at(rwin + lane), rp_n = rp_at(rwin + 32 + lane);
-    float sc = sc_at(rwin + lane), sc_n = sc_at(rwin + 32 + lane);
-    int32_t row_end_e = __shfl_sync(0xffffffffu, rp, 0);
+    int32_t rp = rp_at(rwin + lane), rp_n = rp_at(rwin + G + lane);
+    float sc = sc_at(rwin + lane), sc_n = sc_at(rwin + G + lane);
+    int32_t row_end_e = __shfl_sync(gmask, rp, 0, G);
     float4 acc[NCH], pa[NCH], pm[NCH];
 #pragma unroll
     for (int c = 0; c < NCH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -118,7 +121,7 @@ k_spmm_cpa(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
         if (!EPI) return;
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
-            const int ch = lane + 32 * c;
+            const int ch = lane + G * c;
             if (ch < nchunk && row < r_end) {
                 if (addend)
                     pa[c] = reinterpret_cast<const float4 *>(addend + (int64_t)row * ld_add)[ch];
@@ -128,10 +131,10 @@ k_spmm_cpa(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
         }
     };
     auto close_row = [&]() {
-        const float srow = __shfl_sync(0xffffffffu, sc, row - rwin);
+        const float srow = __shfl_sync(gmask, sc, row - rwin, G);
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
-            const int ch = lane + 32 * c;
+            const int ch = lane + G * c;
             if (ch >= nchunk) continue;
             // explicit roundings (no FMA contraction): every SpMM kernel's epilogue
             // rounds the same way, so they agree bit for bit
@@ -149,14 +152,14 @@ k_spmm_cpa(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
             acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
         ++row;
-        if (row - rwin == 32) {
-            rwin += 32;
+        if (row - rwin == G) {
+            rwin += G;
             rp = rp_n;
             sc = sc_n;
-            rp_n = rp_at(rwin + 32 + lane);
-            sc_n = sc_at(rwin + 32 + lane);
+            rp_n = rp_at(rwin + G + lane);
+            sc_n = sc_at(rwin + G + lane);
         }
-        row_end_e = __shfl_sync(0xffffffffu, rp, row - rwin);
+        row_end_e = __shfl_sync(gmask, rp, row - rwin, G);
         open_row();
     };
     open_row();
@@ -172,9 +175,9 @@ k_spmm_cpa(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
         while (i >= row_end_e) close_row();   // also closes edgeless rows
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
-            const int ch = lane + 32 * c;
+            const int ch = lane + G * c;
             if (ch < nchunk) {
-                const float4 t = ring[(s * NCH + c) * 32 + lane];
+                const float4 t = ring[(s * NCH + c) * G + lane];
                 acc[c].x += t.x; acc[c].y += t.y; acc[c].z += t.z; acc[c].w += t.w;
             }
         }
@@ -184,43 +187,44 @@ k_spmm_cpa(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
     while (row < r_end) close_row();   // trailing rows (incl. edgeless ones)
 }
 
-template <int NCH, int S, bool EPI>
+template <int G, int NCH, int S, bool EPI>
 int launch_epi(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col, int64_t n_direct,
            const int32_t *halo_row, const float *X, int64_t ldx, const float *scale,
            const float *addend, int64_t ld_add, const float *mask, int64_t ld_mask, float *out,
            int64_t ldo, cudaStream_t st) {
-    const size_t smem = (size_t)WARPS * S * NCH * 32 * 16;
+    const size_t smem = (size_t)WARPS * S * NCH * 32 * 16;   // 32/G streams per warp
     static int blocks_per_sm = 0, n_sm = 0;
     if (!blocks_per_sm) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_spmm_cpa<NCH, S, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_spmm_cpa<NCH, S, EPI>,
+        cudaFuncSetAttribute(k_spmm_cpa<G, NCH, S, EPI>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_spmm_cpa<G, NCH, S, EPI>,
                                                       WARPS * 32, smem);
         if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
-    const int64_t warps = (int64_t)n_sm * blocks_per_sm * WARPS;
-    int64_t rpw = (n_rows + warps - 1) / warps;
+    constexpr int SPB = WARPS * 32 / G;   // edge streams per block
+    const int64_t streams = (int64_t)n_sm * blocks_per_sm * SPB;
+    int64_t rpw = (n_rows + streams - 1) / streams;
     if (rpw < 1) rpw = 1;
-    const int64_t blocks = ((n_rows + rpw - 1) / rpw + WARPS - 1) / WARPS;
-    k_spmm_cpa<NCH, S, EPI><<<(unsigned)blocks, WARPS * 32, smem, st>>>(
+    const int64_t blocks = ((n_rows + rpw - 1) / rpw + SPB - 1) / SPB;
+    k_spmm_cpa<G, NCH, S, EPI><<<(unsigned)blocks, WARPS * 32, smem, st>>>(
         n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, scale, addend, ld_add, mask, ld_mask,
         out, ldo, rpw);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 1 : cg_cuda_fail(e, "k_spmm_cpa");
 }
 
-template <int NCH, int S>
+template <int G, int NCH, int S>
 int launch(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col, int64_t n_direct,
            const int32_t *halo_row, const float *X, int64_t ldx, const float *scale,
            const float *addend, int64_t ld_add, const float *mask, int64_t ld_mask, float *out,
            int64_t ldo, cudaStream_t st) {
     return (addend || mask)
-               ? launch_epi<NCH, S, true>(n_rows, F, rowptr, col, n_direct, halo_row, X, ldx,
+               ? launch_epi<G, NCH, S, true>(n_rows, F, rowptr, col, n_direct, halo_row, X, ldx,
                                           scale, addend, ld_add, mask, ld_mask, out, ldo, st)
-               : launch_epi<NCH, S, false>(n_rows, F, rowptr, col, n_direct, halo_row, X, ldx,
+               : launch_epi<G, NCH, S, false>(n_rows, F, rowptr, col, n_direct, halo_row, X, ldx,
                                            scale, addend, ld_add, mask, ld_mask, out, ldo, st);
 }
 
@@ -231,7 +235,7 @@ int launch(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col, int
 // needs the least shared memory.  CG_SPMM_S picks another instantiated depth.
 #define SPMM_CPA_S 4
 
-template <int NCH, int... Ss>
+template <int G, int NCH, int... Ss>
 int launch_s(int S, int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col,
              int64_t n_direct, const int32_t *halo_row, const float *X, int64_t ldx,
              const float *scale, const float *addend, int64_t ld_add, const float *mask,
@@ -239,7 +243,7 @@ int launch_s(int S, int64_t n_rows, int F, const int64_t *rowptr, const int32_t 
     int rc = 0;
     bool hit = false;
     ((S == Ss && !hit
-          ? (hit = true, rc = cpa::launch<NCH, Ss>(n_rows, F, rowptr, col, n_direct, halo_row, X,
+          ? (hit = true, rc = cpa::launch<G, NCH, Ss>(n_rows, F, rowptr, col, n_direct, halo_row, X,
                                                    ldx, scale, addend, ld_add, mask, ld_mask, out,
                                                    ldo, st))
           : 0),
@@ -247,21 +251,22 @@ int launch_s(int S, int64_t n_rows, int F, const int64_t *rowptr, const int32_t 
     return hit ? rc : 0;
 }
 
-// Internal entry: cg_spmm dispatches 128 < F <= 640 here (narrower rows leave
-// lanes idle in a warp-per-edge stream; the register-pipelined kernel's
-// sub-warp groups are faster there).  Returns the launch count, or 0 when
-// this path does not apply (the caller falls back).
+// Internal entry: cg_spmm dispatches sparse-row SpMMs with F <= 640 here
+// (one edge stream per 8 / 16 / 32 lanes by width).  Returns the launch
+// count, or 0 when this path does not apply (the caller falls back).
 int cg_spmm_async(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col,
                   int64_t n_direct, const int32_t *halo_row, const float *X, int64_t ldx,
                   const float *scale, const float *addend, int64_t ld_add, const float *mask,
                   int64_t ld_mask, float *out, int64_t ldo, cudaStream_t st) {
-    if (F <= 128 || F > 640 || F % 4 || ldx % 4) return 0;
+    if (F > 640 || F % 4 || ldx % 4) return 0;
     static const int S = getenv("CG_SPMM_S") ? atoi(getenv("CG_SPMM_S")) : SPMM_CPA_S;
 #define CG_CPA_ARGS n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, scale, addend, ld_add, \
                     mask, ld_mask, out, ldo, st
-    if (F <= 256) return launch_s<2, 3, 4, 6, 8>(S, CG_CPA_ARGS);
-    if (F <= 384) return launch_s<3, 3, 4>(S, CG_CPA_ARGS);
-    if (F <= 512) return launch_s<4, 3, 4>(S, CG_CPA_ARGS);
-    return launch_s<5, 3, 4>(S, CG_CPA_ARGS);
+    if (F <= 64) return launch_s<8, 2, 4, 8>(S, CG_CPA_ARGS);
+    if (F <= 128) return launch_s<16, 2, 4, 8>(S, CG_CPA_ARGS);
+    if (F <= 256) return launch_s<32, 2, 3, 4, 6, 8>(S, CG_CPA_ARGS);
+    if (F <= 384) return launch_s<32, 3, 3, 4>(S, CG_CPA_ARGS);
+    if (F <= 512) return launch_s<32, 4, 3, 4>(S, CG_CPA_ARGS);
+    return launch_s<32, 5, 3, 4>(S, CG_CPA_ARGS);
 #undef CG_CPA_ARGS
 }
