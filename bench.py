@@ -300,8 +300,11 @@ def run_ours(args):
                          "traffic_basis": "per epoch (sum over the k_spmm launches of one "
                                           "epoch, ncu --set full; profiles/spmm_traffic.json), "
                                           "same basis as bytes_per_epoch",
-                         "kernel": "k_spmm (fused cache-lookup + gather SpMM), all fwd+bwd "
-                                   "launches of the timed epochs",
+                         "kernel": "K1/K2 fused cache-lookup + gather SpMM (k_spmm_cpa "
+                                   "cp.async ring for the sparse 128/256-wide launches, "
+                                   "k_spmm for the 40-wide one), all fwd+bwd launches of "
+                                   "the timed epochs; per-launch CUDA-event times from the "
+                                   "epoch graph's event nodes (last timed epoch)",
                          "bytes_per_epoch": sum(fb) + sum(bb),
                          "spmm_ms_per_epoch": tot_ms / args.steps,
                          "launches": [{"pass": ps_, "F": int(w), "bytes": int(b_),
