@@ -270,9 +270,8 @@ class Engine:
 
     def _spmm(self, n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, scale, addend, ld_add,
               mask, ld_mask, out, ldo):
-        """One cg_spmm launch over tensors.  (Splitting it into L2-sized
-        column slices was measured slower on C2: per-row index work grows
-        with the slice count faster than the L2 hit rate pays back.)"""
+        """One cg_spmm call over tensors (the kernel choice and any column
+        slicing happen behind the C ABI)."""
         p = lambda t: None if t is None else ptr(t)  # noqa: E731
         nnz = self.D.nnz_fwd if rowptr is self.fwd_rowptr else self.D.nnz_bwd
         call("cg_spmm", n_rows, F, ptr(rowptr), ptr(col), n_direct, p(halo_row), ptr(X), ldx,
