@@ -80,6 +80,8 @@ struct Params {
     int nbuf;        // staging buffers per epilogue warp (2, or 4 to prefetch masks)
     float *bws;      // weight gradient only: per (chunk, splitter warp) column sums
                      // of the MN-major B operand (= the bias gradient partials)
+    int dbg;         // diagnostics only (CG_GEMM_DBG, wrong results): 1 = splitter
+                     // skips its work, 2 = epilogue skips its stores
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -272,14 +274,20 @@ struct TileCoord {
     int z;
 };
 
+// Tile index -> coordinates.  Tile counts fit 32 bits (m_tiles * n_tiles *
+// chunks < 2^31 for any M < 2^38), so 32-bit divisions suffice; the epilogue's
+// mask-prefetch cursor calls this per 32-column chunk, where 64-bit division
+// chains were the masked GEMM's critical path.
 __device__ __forceinline__ TileCoord tile_of(const Params &p, int64_t t, int n_tiles,
                                              int64_t m_tiles) {
     TileCoord c;
-    const int64_t per_z = m_tiles * n_tiles;
-    c.z = (int)(t / per_z);
-    const int64_t r = t - (int64_t)c.z * per_z;
-    c.m0 = (r / n_tiles) * BM;
-    c.n0 = (int)(r % n_tiles) * p.BN;
+    const uint32_t per_z = (uint32_t)(m_tiles * n_tiles);
+    const uint32_t tt = (uint32_t)t;
+    c.z = (int)(tt / per_z);
+    const uint32_t r = tt - (uint32_t)c.z * per_z;
+    const uint32_t mt = r / (uint32_t)n_tiles;
+    c.m0 = (int64_t)mt * BM;
+    c.n0 = (int)(r - mt * (uint32_t)n_tiles) * p.BN;
     return c;
 }
 
@@ -354,6 +362,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
         // ------------------------------------------------ TMA producer (converged
         // warp; the elected lane issues)
         uint32_t it = 0;
+        int ring_s = 0;        // it % S, kept as a running counter (no divisions)
+        uint32_t ring_ph = 0;  // (it / S) & 1
         for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
             const TileCoord tc = tile_of(p, t, n_tiles, m_tiles);
             for (int o = 0; o < p.n_ops; ++o) {
@@ -364,8 +374,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                 const CUtensorMap *mbl = o ? &mBl1 : &mBl0;
                 const uint32_t bbytes = p.op[o].b_mn ? nb_b * 32 * BK * 4 : p.BN * BK * 4;
                 for (int kb = kb0; kb < kb0 + nkb; ++kb, ++it) {
-                    const int s = it % S;
-                    mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+                    const int s = ring_s;
+                    mbar_wait(&empty[s], ring_ph ^ 1);
+                    if (++ring_s == S) { ring_s = 0; ring_ph ^= 1; }
                     const int k0 = kb * BK;
                     uint8_t *sa = smem + s * stage_bytes;
                     uint8_t *sb = sa + A_BYTES;
@@ -397,6 +408,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
         // ------------------------------------------------ MMA issuer (converged
         // warp; one elected lane issues inside mma_kblock_*; the others idle)
         uint32_t it = 0, ti = 0;
+        int ring_s = 0;
+        uint32_t ring_ph = 0;
         for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++ti) {
             const TileCoord tc = tile_of(p, t, n_tiles, m_tiles);
             const uint32_t acc_buf = ti & 1;
@@ -419,8 +432,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                 const uint32_t a_lay = a_mn ? 1u : 2u, b_lay = b_mn ? 1u : 2u;
                 const uint32_t a_step = a_mn ? 1024 : 32, b_step = b_mn ? 1024 : 32;
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
-                    const int s = it % S;
-                    const uint32_t ph = (it / S) & 1;
+                    const int s = ring_s;
+                    const uint32_t ph = ring_ph;
+                    if (++ring_s == S) { ring_s = 0; ring_ph ^= 1; }
                     if (p.split3) mbar_wait(&conv[s], ph);
                     else mbar_wait(&full[s], ph);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -482,22 +496,26 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
         int64_t pf_t = blockIdx.x;
         int pf_c = 0;
         uint32_t pf_k = 0;
+        TileCoord pc = tile_of(p, pf_t < total_tiles ? pf_t : 0, n_tiles, m_tiles);
         auto pf_issue = [&]() -> bool {
             if (pf_t >= total_tiles) return false;   // sequence exhausted
-            const TileCoord pc = tile_of(p, pf_t, n_tiles, m_tiles);
             if (lane == 0) {
                 asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-                uint64_t *bar = &mbq[pf_k % NB];
+                uint64_t *bar = &mbq[pf_k & (NB - 1)];
                 mbar_expect_tx(bar, EPI_BUF);
-                tma_load_3d(&mM, bar, stg0 + (pf_k % NB) * EPI_BUF, pc.n0 + 32 * pf_c,
+                tma_load_3d(&mM, bar, stg0 + (pf_k & (NB - 1)) * EPI_BUF, pc.n0 + 32 * pf_c,
                             (int)(pc.m0 + 32 * q), 0);
             }
             ++pf_k;
             // advance to the next chunk with columns left
             while (true) {
-                if (++pf_c * 32 >= p.BN) { pf_c = 0; pf_t += gridDim.x; }
+                if (++pf_c * 32 >= p.BN) {
+                    pf_c = 0;
+                    pf_t += gridDim.x;
+                    if (pf_t < total_tiles) pc = tile_of(p, pf_t, n_tiles, m_tiles);
+                }
                 if (pf_t >= total_tiles) break;
-                if (p.N - (tile_of(p, pf_t, n_tiles, m_tiles).n0 + 32 * pf_c) > 0) break;
+                if (p.N - (pc.n0 + 32 * pf_c) > 0) break;
             }
             return true;
         };
@@ -517,7 +535,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                 int ncol = p.N - (tc.n0 + c0);
                 if (ncol > p.BN - c0) ncol = p.BN - c0;
                 if (ncol > 32) ncol = 32;
-                if (p.tma_store && p.tma_mask && ncol > 0) {
+                if (p.tma_store && p.tma_mask && ncol > 0 && !(p.dbg & 2)) {
                     // mask blocks come by TMA into the staging buffers the
                     // chunks will be stored from, D chunks ahead
                     while (pf_k <= nst + D && pf_issue()) {}
@@ -525,13 +543,17 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                 float v[32];
                 tmem_ld32(tmem_base + acc_buf * p.acc_stride + ((uint32_t)(32 * q) << 16) + c0, v);
                 if (ncol <= 0) continue;
+                if (p.dbg & 2) {
+                    if (v[0] == 12345.f) crow[c0] = v[1];   // keep the load live
+                    continue;
+                }
                 if (p.tma_store) {
                     // apply the epilogue in registers, stage the 32 x 32 block
                     // (swizzled: chunk j of row r at j ^ (r & 7)), one TMA store
-                    const uint32_t stg = smem_u32(stg0 + (nst % NB) * EPI_BUF);
+                    const uint32_t stg = smem_u32(stg0 + (nst & (NB - 1)) * EPI_BUF);
                     float4 mk[8];
                     if (p.tma_mask) {
-                        mbar_wait(&mbq[nst % NB], (nst / NB) & 1);
+                        mbar_wait(&mbq[nst & (NB - 1)], (nst >> (31 - __clz(NB))) & 1);
 #pragma unroll
                         for (int j = 0; j < 8; ++j)
                             asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -592,7 +614,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     __syncwarp();
                     if (lane == 0)
-                        tma_store_3d(&mC, stg0 + (nst % NB) * EPI_BUF, tc.n0 + c0,
+                        tma_store_3d(&mC, stg0 + (nst & (NB - 1)) * EPI_BUF, tc.n0 + c0,
                                      (int)(tc.m0 + 32 * q), tc.z);
                     ++nst;
                     continue;
@@ -637,6 +659,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
         // ------------------------------------------------ hi/lo split (3xTF32)
         const int t128 = threadIdx.x - 256;
         uint32_t it = 0;
+        int ring_s = 0;        // it % S, kept as a running counter (no divisions)
+        uint32_t ring_ph = 0;  // (it / S) & 1
         for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
             const TileCoord tc = tile_of(p, t, n_tiles, m_tiles);
             // bias-gradient partials: only the first row tile of each (n, chunk)
@@ -648,8 +672,13 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                 int kb0, nkb;
                 kblocks(p, o, tc.z, kb0, nkb);
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
-                    const int s = it % S;
-                    mbar_wait(&full[s], (it / S) & 1);
+                    const int s = ring_s;
+                    mbar_wait(&full[s], ring_ph);
+                    if (++ring_s == S) { ring_s = 0; ring_ph ^= 1; }
+                    if (p.dbg & 1) {
+                        mbar_arrive(&conv[s]);
+                        continue;
+                    }
                     if (p.a_tmem) {
                         const int q = warp & 3, r = 32 * q + lane;
                         uint32_t hv[32], lv[32];
@@ -839,6 +868,8 @@ int launch(const Params &p0, const CUtensorMap &a0, const CUtensorMap &b0, const
     memset(&mc, 0, sizeof(mc));
     memset(&mm, 0, sizeof(mm));
     static const bool no_tma_store = getenv("CG_GEMM_NO_TMA_STORE") != nullptr;  // experiment knob
+    static const int dbg = getenv("CG_GEMM_DBG") ? atoi(getenv("CG_GEMM_DBG")) : 0;
+    p.dbg = dbg;
     p.tma_store = !no_tma_store && !(p.ldc % 4) && !((uintptr_t)p.C % 16) &&
                   make_map_c(&mc, p.C, p.M, p.N, p.ldc, grid_z);
     p.tma_mask = p.tma_store && p.mask && !(p.ldm % 4) && !((uintptr_t)p.mask % 16) &&
@@ -864,8 +895,13 @@ int launch(const Params &p0, const CUtensorMap &a0, const CUtensorMap &b0, const
         p.acc_stride = BN_MAX;
     }
     const int stage_bytes = p.stage_bytes;
-    // masked epilogues prefetch their mask tiles: 4 staging buffers per warp
-    p.nbuf = p.tma_mask ? 4 : 2;
+    // masked epilogues prefetch their mask tiles NB - 2 chunks ahead: 4 staging
+    // buffers per warp, 8 when K is short (<= 2 k-blocks: the epilogue, not the
+    // MMA, is then the critical path and 2 operand stages suffice)
+    static const int env_nbuf = getenv("CG_GEMM_MASK_NBUF") ? atoi(getenv("CG_GEMM_MASK_NBUF")) : 0;
+    const bool short_k = p.n_ops == 1 && p.op[0].K <= 2 * BK;
+    const bool env_ok = env_nbuf >= 4 && env_nbuf <= 8 && !(env_nbuf & (env_nbuf - 1));  // 4 or 8
+    p.nbuf = p.tma_mask ? (env_ok ? env_nbuf : (short_k ? 8 : 4)) : 2;
     const int smem_fixed = SMEM_BARS + 4 * p.nbuf * EPI_BUF;
     int stages = (SMEM_LIMIT - smem_fixed) / stage_bytes;
     static const int env_stages = getenv("CG_GEMM_STAGES") ? atoi(getenv("CG_GEMM_STAGES")) : 0;
