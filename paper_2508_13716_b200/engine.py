@@ -460,7 +460,10 @@ class Engine:
              ptr(tab_ld), dst if isinstance(dst, int) else ptr(dst), ld, self.stream())
 
     def _gw(self, l: int):
-        if self.c_cpu == 0 or self.L.union is None or self.L.union.size == 0:
+        # compact layout: every read is a version-0 local hit (enforced by the
+        # host tables / K6 flag), so no global entry is ever rewritten
+        if (self.c_cpu == 0 or self.L.union is None or self.L.union.size == 0
+                or self.L.compact):
             return
         F = self.F[l]
         self._copy(self.L.union.size, F, self.gw_src_id, self.gw_src_row, self.gw_slot,
@@ -486,7 +489,7 @@ class Engine:
                 # epoch-1 snapshot of every halo vertex read on this device
                 self._copy(D.n_snap, F, self.snap_src, self.snap_srow, self.snap_dst,
                            self.tab[l], self.tab_ld[l], self.X[l], F)
-            if D.n_halo:
+            if D.n_halo and not self.L.compact:   # compact: nothing is ever staged
                 self._copy(D.n_halo, F, self.stage_src, self.stage_row, self.stage_dst,
                            self.tab[l], self.tab_ld[l], self.X[l], F)
             if spmm_ev is not None:
