@@ -260,8 +260,10 @@ int cg_spmm_async(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *c
                   int64_t ld_mask, float *out, int64_t ldo, cudaStream_t st) {
     if (F > 640 || F % 4 || ldx % 4) return 0;
     static const int S = getenv("CG_SPMM_S") ? atoi(getenv("CG_SPMM_S")) : SPMM_CPA_S;
+    static const bool narrow_g4 = !getenv("CG_SPMM_G4") || atoi(getenv("CG_SPMM_G4")) != 0;
 #define CG_CPA_ARGS n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, scale, addend, ld_add, \
                     mask, ld_mask, out, ldo, st
+    if (F <= 48 && narrow_g4) return launch_s<4, 3, 4, 8>(S, CG_CPA_ARGS);
     if (F <= 64) return launch_s<8, 2, 4, 8>(S, CG_CPA_ARGS);
     if (F <= 128) return launch_s<16, 2, 4, 8>(S, CG_CPA_ARGS);
     if (F <= 256) return launch_s<32, 2, 3, 4, 6, 8>(S, CG_CPA_ARGS);

@@ -29,7 +29,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 python tests/launch_breakdown.py "$OUT/launches.csv" > "$OUT/launches_summary.txt" 2>&1
 
 # one full capture of the SpMM: one epoch worth of launches after warm-up
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_spmm -s 15 -c 5 \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_spmm -s 24 -c 8 \
   -o "$OUT/prof_spmm" python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
   > "$OUT/prof_spmm.log" 2>&1
 if [ -z "${SKIP_GEMM_PROF:-}" ]; then

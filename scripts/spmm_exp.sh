@@ -1,6 +1,6 @@
 set -u
-OUT=gpurun_out/${1:-sx}; mkdir -p $OUT
-CG_SPMM_SLICE=64 timeout 300 python -m pytest tests/test_gpu_train_parity.py -x -q -k "c2" > $OUT/pytest_t.log 2>&1; echo "rc=$?" >> $OUT/pytest_t.log
-for cfg in "0 -1" "128 -1" "64 -1" "64 1"; do set -- $cfg
-if [ "$2" = "-1" ]; then CG_SPMM_SLICE=$1 timeout 300 python bench.py --no-cpu-baseline --steps 20 > $OUT/bench_$1_$2.json 2>> $OUT/bench.err
-else CG_SPMM_SLICE=$1 CG_SPMM_ASYNC=$2 timeout 300 python bench.py --no-cpu-baseline --steps 20 > $OUT/bench_$1_$2.json 2>> $OUT/bench.err; fi; done
+OUT=gpurun_out/${1:-sp}; mkdir -p $OUT
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_spmm -s 24 -c 8 \
+  -o "$OUT/prof_spmm" python bench.py --steps 1 --warmup 3 --no-cpu-baseline > "$OUT/prof_spmm.log" 2>&1
+CG_SPMM_ASYNC=1 timeout 120 python -m pytest tests/test_gpu_kernels.py -x -q -k "spmm" > $OUT/pytest_k.log 2>&1; echo "rc=$?" >> $OUT/pytest_k.log
+for v in 1 0; do CG_SPMM_G4=$v CG_SPMM_ASYNC=1 timeout 300 python bench.py --no-cpu-baseline --steps 20 > $OUT/bench_g4_$v.json 2>> $OUT/bench.err; done

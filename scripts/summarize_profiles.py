@@ -99,8 +99,9 @@ def main(src: str, dst: str):
                        "dram_bytes_per_epoch": tot,
                        "dram_bytes_per_launch": tot / len(rows),
                        "ncu_seconds_per_epoch": dur,
-                       "note": "ncu --set full, one epoch of k_spmm launches (3 fwd + 2 bwd), "
-                               "cold cache, serialised"}
+                       "note": "ncu --set full, one epoch of SpMM launches (k_spmm_cpa / "
+                               "k_spmm: 3 fwd + 2 bwd aggregations, wide ones as 128-column "
+                               "slices = 8 launches on C2), cold cache, serialised"}
     if traffic:
         with open(os.path.join(os.path.dirname(dst.rstrip("/")) or ".", "spmm_traffic.json"),
                   "w") as fh:
