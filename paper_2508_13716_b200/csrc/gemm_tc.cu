@@ -28,6 +28,7 @@
 #include <string>
 
 #include "../../include/capgnn.h"
+#include "pdl.cuh"
 
 extern void cg_set_error(const std::string &msg);
 extern int cg_cuda_fail(cudaError_t e, const char *what);
@@ -355,6 +356,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // barrier init and the TMEM allocation above overlap the previous kernel's
+    // tail; global memory is touched only from here on
+    pdl_entry();
     const uint32_t tmem_base = *tmem_slot;
     const int nb_b = (p.BN + 31) / 32;  // 32-column boxes for an MN-major B
 
@@ -929,7 +933,8 @@ int launch(const Params &p0, const CUtensorMap &a0, const CUtensorMap &b0, const
     }
     const int64_t tiles = (int64_t)((p.N + p.BN - 1) / p.BN) * ((p.M + BM - 1) / BM) * grid_z;
     const unsigned grid = (unsigned)(tiles < n_sm ? tiles : n_sm);   // persistent
-    k_gemm_tc<<<grid, THREADS, smem, st>>>(a0, b0, a1, b1, bl0, bl1, mc, mm, p);
+    cgpdl::launch(k_gemm_tc, dim3(grid), dim3(THREADS), smem, st, a0, b0, a1, b1, bl0, bl1, mc, mm,
+                  p);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 1 : cg_cuda_fail(e, "k_gemm_tc");
 }

@@ -17,6 +17,7 @@
 #include <string>
 
 #include "../../include/capgnn.h"
+#include "pdl.cuh"
 
 extern void cg_set_error(const std::string &msg);
 int cg_spmm_tma(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col,
@@ -86,6 +87,7 @@ __global__ void k_copy_rows(int64_t n, int F, const int32_t *__restrict__ src_id
                             const float *const *__restrict__ tab,
                             const int64_t *__restrict__ tab_ld, float *__restrict__ dst,
                             int64_t ld_dst) {
+    pdl_entry();
     // Each warp scans 32 table entries at a time (one per lane), compacts the
     // live ones with a ballot, then copies those rows cooperatively: most
     // epochs most entries are "nothing to move" (stale local hits).
@@ -156,6 +158,7 @@ k_spmm(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
        const float *__restrict__ X, int64_t ldx, const float *__restrict__ scale,
        const float *__restrict__ addend, int64_t ld_add, const float *__restrict__ mask,
        int64_t ld_mask, float *__restrict__ out, int64_t ldo) {
+    pdl_entry();
     constexpr int UNR = (NCH == 1) ? SPMM_UNR1 : SPMM_UNR2;   // rows in flight per lane
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -309,6 +312,7 @@ __global__ void __launch_bounds__(256)
 k_softmax_ce4(int64_t n, int C, const float *__restrict__ logits, int64_t ld,
               const int32_t *__restrict__ label, float inv_n, float *__restrict__ grad,
               int64_t ldg, float *__restrict__ block_loss) {
+    pdl_entry();
     __shared__ float wl[8];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int sub = lane & 3;                       // lane within the row group
@@ -384,6 +388,7 @@ k_softmax_ce4(int64_t n, int C, const float *__restrict__ logits, int64_t ld,
 
 // Deterministic sum of x[0..n) into *out (single block, fixed order).
 __global__ void k_sum_fixed(const float *__restrict__ x, int64_t n, float *__restrict__ out) {
+    pdl_entry();
     __shared__ double sh[1024];
     double s = 0.0;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += (double)x[i];
@@ -498,6 +503,7 @@ __global__ void __launch_bounds__(NW * 32)
 k_reduce_chunks_pair4(int64_t nb1, int64_t n1, int64_t c1, const float *__restrict__ ws1,
                       float *__restrict__ out1, int64_t n2, int64_t c2,
                       const float *__restrict__ ws2, float *__restrict__ out2) {
+    pdl_entry();
     if (blockIdx.x < nb1) reduce_chunks_block4<NW>(blockIdx.x, n1, c1, ws1, out1);
     else reduce_chunks_block4<NW>(blockIdx.x - nb1, n2, c2, ws2, out2);
 }
@@ -574,6 +580,7 @@ __global__ void k_scale_rows_to(float *__restrict__ dst, int64_t ldd, const floa
 // float4 variant (F, ldd, lds multiples of 4, 16-byte aligned rows)
 __global__ void k_scale_rows_to4(float *__restrict__ dst, int64_t ldd, const float *__restrict__ src,
                                  int64_t lds, int64_t n, int F4, const float *__restrict__ scale) {
+    pdl_entry();
     const int64_t total = n * (int64_t)F4;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -604,6 +611,7 @@ __global__ void k_adam(int64_t n, float *__restrict__ p, const float *__restrict
                        float *__restrict__ m, float *__restrict__ v, float lr, float b1,
                        float b2, float eps, float c1_arg, float c2_arg, float *__restrict__ p_hi,
                        float *__restrict__ p_lo, const float *__restrict__ corr_dev) {
+    pdl_entry();
     // bias corrections: arguments, or device-resident under graph replay
     const float c1 = corr_dev ? corr_dev[0] : c1_arg, c2 = corr_dev ? corr_dev[1] : c2_arg;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -628,6 +636,7 @@ __global__ void k_adam(int64_t n, float *__restrict__ p, const float *__restrict
 __global__ void k_split_tf32_t(const int64_t *__restrict__ off, const int32_t *__restrict__ rows,
                                const int32_t *__restrict__ cols, const float *__restrict__ x,
                                float *__restrict__ hi, float *__restrict__ lo) {
+    pdl_entry();
     const int m = blockIdx.y;
     const int64_t o = off[m];
     const int r = rows[m], c = cols[m];
@@ -754,6 +763,7 @@ k_plan_frozen(cg_plan_static st, int e_arg, int s, int me, int32_t *req_ver,
               int32_t *stage_row, int32_t *stage_dst, int32_t *gw_slot,
               int64_t *counts, int32_t *flag, int32_t staging_base,
               int32_t n_devices, int8_t *outcome, const int32_t *epoch_dev) {
+    pdl_entry();
     const int e = epoch_dev ? *epoch_dev : e_arg;   // device-resident under graph replay
     // outcome counters: shared-memory tallies, one global add per block
     __shared__ unsigned int tally[3 * kPlanMaxParts];
@@ -797,8 +807,8 @@ int cg_reduce_chunks_pair(int64_t n1, int64_t c1, const float *ws1, float *out1,
     if (n1 % 4 == 0 && n2 % 4 == 0 && al(ws1) && al(out1) && (n2 == 0 || (al(ws2) && al(out2)))) {
         const int64_t b1 = (n1 / 4 + 31) / 32, b2 = (n2 / 4 + 31) / 32;
         if (b1 + b2 == 0) return 0;
-        k_reduce_chunks_pair4<8><<<(unsigned)(b1 + b2), 256, 0, st>>>(b1, n1, c1, ws1, out1, n2,
-                                                                       c2, ws2, out2);
+        cgpdl::launch(k_reduce_chunks_pair4<8>, dim3((unsigned)(b1 + b2)), dim3(256), 0, st, b1,
+                      n1, c1, ws1, out1, n2, c2, ws2, out2);
         CG_CHECK_LAUNCH("k_reduce_chunks_pair4");
         return 1;
     }
@@ -855,11 +865,11 @@ int cg_copy_rows(int64_t n, int F, const int32_t *src_id, const int32_t *src_row
     bool vec = (F % 4 == 0) && (ld_dst % 4 == 0) && ((uintptr_t)dst % 16 == 0);
     // source alignment is validated on the host side (tab_ld % 4 == 0, 16-B bases)
     if (vec)
-        k_copy_rows<true><<<blocks, threads, 0, (cudaStream_t)stream>>>(
-            n, F, src_id, src_row, dst_row, tab, tab_ld, dst, ld_dst);
+        cgpdl::launch(k_copy_rows<true>, dim3(blocks), dim3(threads), 0, (cudaStream_t)stream, n,
+                      F, src_id, src_row, dst_row, tab, tab_ld, dst, ld_dst);
     else
-        k_copy_rows<false><<<blocks, threads, 0, (cudaStream_t)stream>>>(
-            n, F, src_id, src_row, dst_row, tab, tab_ld, dst, ld_dst);
+        cgpdl::launch(k_copy_rows<false>, dim3(blocks), dim3(threads), 0, (cudaStream_t)stream, n,
+                      F, src_id, src_row, dst_row, tab, tab_ld, dst, ld_dst);
     CG_CHECK_LAUNCH("k_copy_rows");
     return 1;
 }
@@ -975,9 +985,10 @@ int cg_spmm(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col, in
                                                           threads, 0);                      \
             if (blocks_per_sm < 1) blocks_per_sm = 1;                                       \
         }                                                                                   \
-        k_spmm<G, NCH><<<grid_for(n_rows * G, threads, n_sms() * blocks_per_sm), threads, 0, \
-                         st>>>(n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, scale,  \
-                               addend, ld_add, mask, ld_mask, out, ldo);                    \
+        cgpdl::launch(k_spmm<G, NCH>,                                                        \
+                      dim3(grid_for(n_rows * G, threads, n_sms() * blocks_per_sm)),          \
+                      dim3(threads), 0, st, n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, \
+                      scale, addend, ld_add, mask, ld_mask, out, ldo);                       \
     } while (0)
     if (nchunk <= 8) CG_SPMM_LAUNCH(8, 1);
     else if (nchunk <= 16) CG_SPMM_LAUNCH(16, 1);
@@ -1008,8 +1019,9 @@ int cg_scale_rows_to(float *dst, int64_t ldd, const float *src, int64_t lds, int
                      int F, const float *scale, void *stream) {
     if (n_rows == 0 || F == 0) return 0;
     if (!(F % 4) && !(ldd % 4) && !(lds % 4) && !((uintptr_t)dst % 16) && !((uintptr_t)src % 16)) {
-        k_scale_rows_to4<<<grid_for(n_rows * (F / 4), 256, n_sms() * 8), 256, 0,
-                           (cudaStream_t)stream>>>(dst, ldd, src, lds, n_rows, F / 4, scale);
+        cgpdl::launch(k_scale_rows_to4, dim3(grid_for(n_rows * (F / 4), 256, n_sms() * 8)),
+                      dim3(256), 0, (cudaStream_t)stream, dst, ldd, src, lds, n_rows, F / 4,
+                      scale);
         CG_CHECK_LAUNCH("k_scale_rows_to4");
         return 1;
     }
@@ -1041,16 +1053,16 @@ int cg_softmax_ce(int64_t n_rows, int C, const float *logits, int64_t ld, const 
     if (narrow) {
         blocks = grid_for(n_rows * 4, 256, n_sms() * 8);
         if (C <= 32)
-            k_softmax_ce4<2><<<blocks, 256, 0, st>>>(n_rows, C, logits, ld, label, inv_n, grad,
-                                                     ldg, ws);
+            cgpdl::launch(k_softmax_ce4<2>, dim3(blocks), dim3(256), 0, st, n_rows, C, logits, ld,
+                          label, inv_n, grad, ldg, ws);
         else
-            k_softmax_ce4<4><<<blocks, 256, 0, st>>>(n_rows, C, logits, ld, label, inv_n, grad,
-                                                     ldg, ws);
+            cgpdl::launch(k_softmax_ce4<4>, dim3(blocks), dim3(256), 0, st, n_rows, C, logits, ld,
+                          label, inv_n, grad, ldg, ws);
     } else {
         blocks = grid_for(n_rows * 32, 256, 148 * 8);
         k_softmax_ce<<<blocks, 256, 0, st>>>(n_rows, C, logits, ld, label, inv_n, grad, ldg, ws);
     }
-    k_sum_fixed<<<1, 1024, 0, st>>>(ws, blocks, loss_out);
+    cgpdl::launch(k_sum_fixed, dim3(1), dim3(1024), 0, st, ws, (int64_t)blocks, loss_out);
     CG_CHECK_LAUNCH("cg_softmax_ce");
     return 2;
 }
@@ -1070,13 +1082,14 @@ int cg_adam(int64_t n, float *param, const float *grad, float *m, float *v, floa
     }
     float c1, c2;
     adam_corrections(beta1, beta2, step, &c1, &c2);
-    k_adam<<<grid_for(n, 256, 148 * 8), 256, 0, (cudaStream_t)stream>>>(
-        n, param, grad, m, v, lr, beta1, beta2, eps, c1, c2, p_hi, p_lo, corr_dev);
+    cgpdl::launch(k_adam, dim3(grid_for(n, 256, 148 * 8)), dim3(256), 0, (cudaStream_t)stream, n,
+                  param, grad, m, v, lr, beta1, beta2, eps, c1, c2, p_hi, p_lo, corr_dev);
     CG_CHECK_LAUNCH("k_adam");
     return 1;
 }
 
 __global__ void k_set_epoch(int32_t *epoch_dev, int epoch, float *corr_dev, float c1, float c2) {
+    pdl_entry();
     *epoch_dev = epoch;
     if (corr_dev) {
         corr_dev[0] = c1;
@@ -1088,7 +1101,8 @@ int cg_set_epoch(int32_t *epoch_dev, int epoch, float *corr_dev, float beta1, fl
                  int step, void *stream) {
     float c1, c2;
     adam_corrections(beta1, beta2, step, &c1, &c2);
-    k_set_epoch<<<1, 1, 0, (cudaStream_t)stream>>>(epoch_dev, epoch, corr_dev, c1, c2);
+    cgpdl::launch(k_set_epoch, dim3(1), dim3(1), 0, (cudaStream_t)stream, epoch_dev, epoch,
+                  corr_dev, c1, c2);
     CG_CHECK_LAUNCH("k_set_epoch");
     return 1;
 }
@@ -1109,7 +1123,8 @@ int cg_split_tf32_t(int n_mats, const int64_t *off, const int32_t *rows, const i
                     const float *x, float *hi, float *lo, int64_t max_elems, void *stream) {
     if (n_mats == 0 || max_elems == 0) return 0;
     dim3 grid((unsigned)((max_elems + 255) / 256), (unsigned)n_mats);
-    k_split_tf32_t<<<grid, 256, 0, (cudaStream_t)stream>>>(off, rows, cols, x, hi, lo);
+    cgpdl::launch(k_split_tf32_t, grid, dim3(256), 0, (cudaStream_t)stream, off, rows, cols, x,
+                  hi, lo);
     CG_CHECK_LAUNCH("k_split_tf32_t");
     return 1;
 }
@@ -1131,9 +1146,10 @@ int cg_plan_frozen(const cg_plan_static *st, int epoch, int staleness, int me, i
         cg_set_error("cg_plan_frozen: too many partition slots");
         return -1;
     }
-    k_plan_frozen<<<(unsigned)((st->n_union + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-        *st, epoch, staleness, me, req_ver, glob_ver, halo_row, stage_src, stage_row, stage_dst,
-        gw_slot, counts, flag, staging_base, n_devices, outcome, epoch_dev);
+    cgpdl::launch(k_plan_frozen, dim3((unsigned)((st->n_union + 255) / 256)), dim3(256), 0,
+                  (cudaStream_t)stream, *st, epoch, staleness, me, req_ver, glob_ver, halo_row,
+                  stage_src, stage_row, stage_dst, gw_slot, counts, flag, staging_base, n_devices,
+                  outcome, epoch_dev);
     CG_CHECK_LAUNCH("k_plan_frozen");
     return 1;
 }

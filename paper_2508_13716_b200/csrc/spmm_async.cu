@@ -19,6 +19,8 @@
 #include <cstdlib>
 #include <string>
 
+#include "pdl.cuh"
+
 extern void cg_set_error(const std::string &msg);
 extern int cg_cuda_fail(cudaError_t e, const char *what);
 
@@ -48,6 +50,7 @@ k_spmm_cpa(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
            const float *__restrict__ addend, int64_t ld_add, const float *__restrict__ mask,
            int64_t ld_mask, float *__restrict__ out, int64_t ldo, int64_t rows_per_warp) {
     extern __shared__ __align__(16) float4 ring_all[];
+    pdl_entry();
     const int grp = threadIdx.x / G, lane = threadIdx.x & (G - 1);
     const unsigned gmask = G == 32 ? 0xffffffffu
                                    : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
@@ -209,9 +212,9 @@ int launch_epi(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col,
     int64_t rpw = (n_rows + streams - 1) / streams;
     if (rpw < 1) rpw = 1;
     const int64_t blocks = ((n_rows + rpw - 1) / rpw + SPB - 1) / SPB;
-    k_spmm_cpa<G, NCH, S, EPI><<<(unsigned)blocks, WARPS * 32, smem, st>>>(
-        n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, scale, addend, ld_add, mask, ld_mask,
-        out, ldo, rpw);
+    cgpdl::launch(k_spmm_cpa<G, NCH, S, EPI>, dim3((unsigned)blocks), dim3(WARPS * 32), smem, st,
+                  n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, scale, addend, ld_add, mask,
+                  ld_mask, out, ldo, rpw);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 1 : cg_cuda_fail(e, "k_spmm_cpa");
 }
