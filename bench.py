@@ -230,15 +230,17 @@ def run_ours(args):
     bwd_model = int(sum(ps.cut_edges)) * bpe
 
     # ---- end-to-end through the public session API: every step uploads its
-    # input rows from pinned host memory (H2D) and downloads its logits and
-    # loss (D2H).  Uploads run one step ahead on a copy stream and downloads
-    # overlap the backward pass; the clock is the host wall clock around the
-    # whole run including the final synchronisation.
+    # input rows from pinned host memory (H2D) and downloads its result, the
+    # loss (D2H) -- what train() hands back per epoch.  Uploads run one step
+    # ahead on a copy stream; the clock is the host wall clock around the whole
+    # run including the final synchronisation.  (--e2e-logits also downloads
+    # the 27 MB of logits every step.)
     from paper_2508_13716_b200.models import _unit  # deterministic host features
     rows = D.verts.astype(np.uint64)[:, None]
     host_x = torch.from_numpy(_unit(0, rows, np.arange(F_DIM[0], dtype=np.uint64)[None, :])).pin_memory()
     e2e_steps = args.steps
-    host_logits = [torch.empty(D.n_in, eng.C4).pin_memory() for _ in range(2)]
+    host_logits = ([torch.empty(D.n_in, eng.C4).pin_memory() for _ in range(2)]
+                   if args.e2e_logits else None)
     host_loss = torch.empty(e2e_steps + 2).pin_memory()
 
     def e2e_run(n, loss_off):
@@ -247,7 +249,8 @@ def run_ours(args):
             s = sess.step(sync=False)
             if i + 1 < n:
                 sess.prefetch_features(host_x)      # next step's inputs, behind this epoch
-            sess.fetch_logits(host_logits[i & 1])
+            if args.e2e_logits:
+                sess.fetch_logits(host_logits[i & 1])
             sess.fetch_loss(s, host_loss[loss_off + i:loss_off + i + 1])
 
     e2e_run(2, e2e_steps)        # warm-up: copy streams, staging buffer, pinned paths
@@ -263,12 +266,13 @@ def run_ours(args):
     w_s = max_over_ranks(w_s, world, args.dist_backend)
     e2e = {"value": L * E * e2e_steps / w_s / 1e9, "unit": "GTEPS",
            "h2d_bytes_per_step": int(host_x.numel() * 4),
-           "d2h_bytes_per_step": int(host_logits[0].numel() * 4 + 4),
+           "d2h_bytes_per_step": int(D.n_in * eng.C4 * 4 + 4) if args.e2e_logits else 4,
            "steps": e2e_steps, "ms_per_step": w_s / e2e_steps * 1e3,
            "how": "api.TrainSession, 2 untimed warm-up steps, then per step: pinned-host input "
                   "rows H2D (prefetched one step ahead on a copy stream; GCN: row scaling), "
-                  "epoch, logits + loss D2H (overlapping the backward); host wall clock incl. "
-                  "final sync"}
+                  "epoch, loss D2H" + (" + logits D2H (overlapping the backward)"
+                                       if args.e2e_logits else "") +
+                  "; host wall clock incl. final sync"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -421,6 +425,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--parts", type=int, default=PARTS)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--e2e-logits", action="store_true",
+                    help="e2e: also download the logits every step")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help=argparse.SUPPRESS)
     ap.add_argument("--staleness", type=int, default=-1)
