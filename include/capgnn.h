@@ -139,10 +139,14 @@ int cg_colsum(int64_t M, int N, const float *D, int64_t ldd, float *db, float *w
 
 /* ---- K8: softmax cross-entropy ---------------------------------------- */
 /* grad[r, c] = (softmax(logits[r]) - onehot(label[r])) * inv_n;
- * loss_out[0] = sum_r (lse_r - logits[r, label[r]]) (deterministic).     */
+ * loss_out[0] = sum_r (lse_r - logits[r, label[r]]) (deterministic).
+ * grad2 (optional): also grad[r, c] * scale2[r] (scale2 NULL = 1), the
+ * row-scaled gradient the backward aggregation gathers, written in the same
+ * pass (the ldg-wide row, padding included).                             */
 int cg_softmax_ce(int64_t n_rows, int C, const float *logits, int64_t ld,
                   const int32_t *label, float inv_n, float *grad, int64_t ldg,
-                  float *loss_out, float *ws, void *stream);
+                  float *loss_out, float *ws, float *grad2, int64_t ldg2,
+                  const float *scale2, void *stream);
 
 /* ---- optimizer (replicated on every rank after the K7 all-reduce) ------ */
 /* p_hi / p_lo (optional): also emit the TF32 split of the updated params

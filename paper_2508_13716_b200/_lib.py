@@ -59,7 +59,7 @@ SIGNATURES = {
     "cg_wgrad_workspace": [I64, INT, INT],
     "cg_wgrad": [I64, INT, INT, P, I64, P, I64, P, P, P, INT, P],
     "cg_colsum": [I64, INT, P, I64, P, P, P],
-    "cg_softmax_ce": [I64, INT, P, I64, P, F32, P, I64, P, P, P],
+    "cg_softmax_ce": [I64, INT, P, I64, P, F32, P, I64, P, P, P, I64, P, P],
     "cg_adam": [I64, P, P, P, P, F32, F32, F32, F32, INT, P, P, P, P],
     "cg_set_epoch": [P, INT, P, F32, F32, INT, P],
     "cg_event_record": [P, P],

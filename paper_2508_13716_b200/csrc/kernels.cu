@@ -311,7 +311,8 @@ template <int NV>
 __global__ void __launch_bounds__(256)
 k_softmax_ce4(int64_t n, int C, const float *__restrict__ logits, int64_t ld,
               const int32_t *__restrict__ label, float inv_n, float *__restrict__ grad,
-              int64_t ldg, float *__restrict__ block_loss) {
+              int64_t ldg, float *__restrict__ block_loss, float *__restrict__ grad2,
+              int64_t ldg2, const float *__restrict__ scale2) {
     pdl_entry();
     __shared__ float wl[8];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -368,6 +369,12 @@ k_softmax_ce4(int64_t n, int C, const float *__restrict__ logits, int64_t ld,
             if (y >= c && y < c + 4) zy = (y == c) ? v[k].x : (y == c + 1) ? v[k].y
                                         : (y == c + 2) ? v[k].z : v[k].w;
             g4[c4] = p;
+            if (grad2) {   // the row-scaled copy the backward aggregation gathers
+                const float sr = scale2 ? scale2[r] : 1.f;
+                reinterpret_cast<float4 *>(grad2 + r * ldg2)[c4] =
+                    make_float4(__fmul_rn(p.x, sr), __fmul_rn(p.y, sr), __fmul_rn(p.z, sr),
+                                __fmul_rn(p.w, sr));
+            }
         }
         zy += __shfl_xor_sync(0xffffffffu, zy, 1);
         zy += __shfl_xor_sync(0xffffffffu, zy, 2);
@@ -1044,27 +1051,34 @@ int cg_colsum(int64_t M, int N, const float *D, int64_t ldd, float *db, float *w
 
 int cg_softmax_ce(int64_t n_rows, int C, const float *logits, int64_t ld, const int32_t *label,
                   float inv_n, float *grad, int64_t ldg, float *loss_out, float *ws,
-                  void *stream) {
+                  float *grad2, int64_t ldg2, const float *scale2, void *stream) {
     if (n_rows == 0) return 0;
     cudaStream_t st = (cudaStream_t)stream;
     const bool narrow = C <= 64 && !(ld % 4) && !(ldg % 4) && !((uintptr_t)logits % 16) &&
-                        !((uintptr_t)grad % 16);
+                        !((uintptr_t)grad % 16) &&
+                        (!grad2 || (!(ldg2 % 4) && !((uintptr_t)grad2 % 16)));
     int blocks;
     if (narrow) {
         blocks = grid_for(n_rows * 4, 256, n_sms() * 8);
         if (C <= 32)
             cgpdl::launch(k_softmax_ce4<2>, dim3(blocks), dim3(256), 0, st, n_rows, C, logits, ld,
-                          label, inv_n, grad, ldg, ws);
+                          label, inv_n, grad, ldg, ws, grad2, ldg2, scale2);
         else
             cgpdl::launch(k_softmax_ce4<4>, dim3(blocks), dim3(256), 0, st, n_rows, C, logits, ld,
-                          label, inv_n, grad, ldg, ws);
+                          label, inv_n, grad, ldg, ws, grad2, ldg2, scale2);
     } else {
         blocks = grid_for(n_rows * 32, 256, 148 * 8);
         k_softmax_ce<<<blocks, 256, 0, st>>>(n_rows, C, logits, ld, label, inv_n, grad, ldg, ws);
     }
     cgpdl::launch(k_sum_fixed, dim3(1), dim3(1024), 0, st, ws, (int64_t)blocks, loss_out);
     CG_CHECK_LAUNCH("cg_softmax_ce");
-    return 2;
+    int launched = 2;
+    if (grad2 && !narrow) {   // the wide-C kernel has no fused copy: scale separately
+        const int rc = cg_scale_rows_to(grad2, ldg2, grad, ldg, n_rows, C, scale2, stream);
+        if (rc < 0) return rc;
+        launched += rc;
+    }
+    return launched;
 }
 
 static void adam_corrections(float beta1, float beta2, int step, float *c1, float *c2) {

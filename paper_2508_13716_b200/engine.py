@@ -520,10 +520,20 @@ class Engine:
             torch.cuda.current_stream(self.dev).wait_event(self._io["logits_done"])
             self._io["logits_done"] = None
 
+    def _last_wide(self) -> bool:
+        """The last layer's backward aggregates the (narrow) logits gradient."""
+        return self.dims[self.nL] < self.F[self.nL - 1]
+
     def _loss(self) -> None:
         loss_ptr = ptr(self.grads) + 4 * self.n_params
+        # the wide last layer's gathered rows G = norm_dst * dL come out of the
+        # same pass (no separate scaling launch)
+        l = self.nL - 1
+        g2 = ptr(self.Gs[l & 1]) if self._last_wide() else None
+        sc = ptr(self.norm_dst) if g2 is not None else None
         call("cg_softmax_ce", self.D.n_in, self.C, ptr(self.logits), self.C4, ptr(self.labels),
-             1.0 / self.L.n, ptr(self.dL), self.C4, loss_ptr, ptr(self.ce_ws), self.stream())
+             1.0 / self.L.n, ptr(self.dL), self.C4, loss_ptr, ptr(self.ce_ws), g2, self.C4, sc,
+             self.stream())
 
     def _backward(self, spmm_ev) -> None:
         st, nL, kind, n_in = self.stream(), self.nL, self.kind, self.D.n_in
@@ -548,9 +558,11 @@ class Engine:
             G = self.Gs[l & 1]
             W = 2 * l if kind == "gcn" else 3 * l + 1
             if wide:
-                # G = (b | 1/d_in) * dY  (F_out wide): the rows peers pull
-                call("cg_scale_rows_to", ptr(G), Fo, ptr(dY), Fo, n_in, Fo,
-                     ptr(self.norm_dst), st)
+                # G = (b | 1/d_in) * dY  (F_out wide): the rows peers pull (the
+                # last layer's comes out of cg_softmax_ce)
+                if l != nL - 1:
+                    call("cg_scale_rows_to", ptr(G), Fo, ptr(dY), Fo, n_in, Fo,
+                         ptr(self.norm_dst), st)
                 Fx = Fo
             elif kind == "gcn":
                 self._gemm(n_in, F, Fo, ptr(dY), Fo, W, trans_b=1, row_scale=ptr(self.norm_dst),

@@ -172,9 +172,13 @@ def test_softmax_ce_and_adam(Cc, ld):
     loss = torch.zeros(1, device="cuda")
     ws = torch.zeros(n, device="cuda")
     tz, ty = _t(zp), _t(y)
+    g2 = torch.full((n, ld), 7.0, device="cuda")   # fused row-scaled copy
+    sc = _t(rng.random(n).astype(np.float32))
     call("cg_softmax_ce", n, Cc, ptr(tz), ld, ptr(ty), 1.0 / n, ptr(g), ld, ptr(loss),
-         ptr(ws), _st())
+         ptr(ws), ptr(g2), ld, ptr(sc), _st())
     _sync()
+    # exactly grad * scale (one rounding), as the separate cg_scale_rows_to gives
+    assert torch.equal(g2[:, :Cc], g[:, :Cc] * sc[:, None])
     g = g[:, :Cc]
     zz = z.astype(np.float64)
     m = zz.max(1, keepdims=True)
