@@ -814,8 +814,18 @@ int cg_reduce_chunks_pair(int64_t n1, int64_t c1, const float *ws1, float *out1,
     if (n1 % 4 == 0 && n2 % 4 == 0 && al(ws1) && al(out1) && (n2 == 0 || (al(ws2) && al(out2)))) {
         const int64_t b1 = (n1 / 4 + 31) / 32, b2 = (n2 / 4 + 31) / 32;
         if (b1 + b2 == 0) return 0;
-        cgpdl::launch(k_reduce_chunks_pair4<8>, dim3((unsigned)(b1 + b2)), dim3(256), 0, st, b1,
-                      n1, c1, ws1, out1, n2, c2, ws2, out2);
+        // warps per block so the launch fills the GPU (few outputs, many chunks:
+        // a 256 x 40 dW has 148 chunks over 81 blocks)
+        const int64_t want = (int64_t)n_sms() * 32 / (b1 + b2);
+        if (want >= 32)
+            cgpdl::launch(k_reduce_chunks_pair4<32>, dim3((unsigned)(b1 + b2)), dim3(1024), 0, st,
+                          b1, n1, c1, ws1, out1, n2, c2, ws2, out2);
+        else if (want >= 16)
+            cgpdl::launch(k_reduce_chunks_pair4<16>, dim3((unsigned)(b1 + b2)), dim3(512), 0, st,
+                          b1, n1, c1, ws1, out1, n2, c2, ws2, out2);
+        else
+            cgpdl::launch(k_reduce_chunks_pair4<8>, dim3((unsigned)(b1 + b2)), dim3(256), 0, st,
+                          b1, n1, c1, ws1, out1, n2, c2, ws2, out2);
         CG_CHECK_LAUNCH("k_reduce_chunks_pair4");
         return 1;
     }
