@@ -142,7 +142,9 @@ int cg_colsum(int64_t M, int N, const float *D, int64_t ldd, float *db, float *w
  * loss_out[0] = sum_r (lse_r - logits[r, label[r]]) (deterministic).
  * grad2 (optional): also grad[r, c] * scale2[r] (scale2 NULL = 1), the
  * row-scaled gradient the backward aggregation gathers, written in the same
- * pass (the ldg-wide row, padding included).                             */
+ * pass (the ldg-wide row, padding included).
+ * ws: >= n_rows + 1 floats, zeroed by the caller once (the kernel re-arms the
+ * finish ticket it keeps there).                                         */
 int cg_softmax_ce(int64_t n_rows, int C, const float *logits, int64_t ld,
                   const int32_t *label, float inv_n, float *grad, int64_t ldg,
                   float *loss_out, float *ws, float *grad2, int64_t ldg2,

@@ -312,7 +312,8 @@ __global__ void __launch_bounds__(256)
 k_softmax_ce4(int64_t n, int C, const float *__restrict__ logits, int64_t ld,
               const int32_t *__restrict__ label, float inv_n, float *__restrict__ grad,
               int64_t ldg, float *__restrict__ block_loss, float *__restrict__ grad2,
-              int64_t ldg2, const float *__restrict__ scale2) {
+              int64_t ldg2, const float *__restrict__ scale2, float *__restrict__ loss_out,
+              unsigned int *__restrict__ ticket) {
     pdl_entry();
     __shared__ float wl[8];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -385,11 +386,31 @@ k_softmax_ce4(int64_t n, int C, const float *__restrict__ logits, int64_t ld,
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) wl[w] = acc;
     __syncthreads();
+    __shared__ bool last;
     if (threadIdx.x == 0) {
         float t = 0.f;
 #pragma unroll
         for (int k = 0; k < 8; ++k) t += wl[k];
         block_loss[blockIdx.x] = t;
+        // the last block to finish sums the block partials (fixed order, as
+        // k_sum_fixed did in a launch of its own) and re-arms the ticket
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __shared__ double sh[256];
+    double t = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) t += (double)__ldcg(block_loss + i);
+    sh[threadIdx.x] = t;
+    __syncthreads();
+    for (int k = blockDim.x / 2; k > 0; k >>= 1) {
+        if (threadIdx.x < k) sh[threadIdx.x] += sh[threadIdx.x + k];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        *loss_out = (float)sh[0];
+        *ticket = 0u;
     }
 }
 
@@ -1070,12 +1091,17 @@ int cg_softmax_ce(int64_t n_rows, int C, const float *logits, int64_t ld, const 
     int blocks;
     if (narrow) {
         blocks = grid_for(n_rows * 4, 256, n_sms() * 8);
+        // ws[0, blocks): block partials; the word after them: the finish ticket
+        // (zero on entry: the caller's zeroed workspace, re-armed by each launch)
+        unsigned int *ticket = reinterpret_cast<unsigned int *>(ws + blocks);
         if (C <= 32)
             cgpdl::launch(k_softmax_ce4<2>, dim3(blocks), dim3(256), 0, st, n_rows, C, logits, ld,
-                          label, inv_n, grad, ldg, ws, grad2, ldg2, scale2);
+                          label, inv_n, grad, ldg, ws, grad2, ldg2, scale2, loss_out, ticket);
         else
             cgpdl::launch(k_softmax_ce4<4>, dim3(blocks), dim3(256), 0, st, n_rows, C, logits, ld,
-                          label, inv_n, grad, ldg, ws, grad2, ldg2, scale2);
+                          label, inv_n, grad, ldg, ws, grad2, ldg2, scale2, loss_out, ticket);
+        CG_CHECK_LAUNCH("cg_softmax_ce");
+        return 1;
     } else {
         blocks = grid_for(n_rows * 32, 256, 148 * 8);
         k_softmax_ce<<<blocks, 256, 0, st>>>(n_rows, C, logits, ld, label, inv_n, grad, ldg, ws);

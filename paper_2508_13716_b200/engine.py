@@ -155,7 +155,7 @@ class Engine:
             ws = max(ws, call("cg_wgrad_workspace", D.n_in, dims[l], dims[l + 1]),
                      (D.n_in + 255) // 256 * dims[l + 1])  # cg_colsum: 256-row chunks
         self.ws = torch.zeros(ws, dtype=f32, device=dev)
-        self.ce_ws = torch.zeros(max(D.n_in, 1), dtype=f32, device=dev)
+        self.ce_ws = torch.zeros(max(D.n_in, 1) + 1, dtype=f32, device=dev)   # + finish ticket
         # graph structure
         self.fwd_rowptr = _dev(D.fwd_rowptr, i64, dev)
         self.fwd_col = _dev(D.fwd_col, i32, dev)
