@@ -729,7 +729,12 @@ __device__ __forceinline__ void plan_vertex(const cg_plan_static &st, int64_t u,
                 *flag = 1;
         }
         if (outcome) outcome[k] = (int8_t)oc;
-        atomicAdd(&tally[3 * part + oc], 1u);
+        {   // warp-aggregated tally: one shared atomic per distinct (part, outcome)
+            const unsigned am = __activemask();
+            const int key = 3 * part + oc;
+            const unsigned peers = __match_any_sync(am, key);
+            if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&tally[key], __popc(peers));
+        }
         if (st.req_dev[k] != me) continue;
         const int32_t pos = st.req_pos[k];
         const bool cur = (ver < 1 ? 1 : ver) == e;
