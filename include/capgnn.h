@@ -74,14 +74,6 @@ int cg_scale_rows_to(float *dst, int64_t ldd, const float *src, int64_t lds, int
  * dst may itself be a peer or host-tier pointer (write-through).
  * Replaces the data movement behind CacheSystem.lookup outcomes
  * (cache.py:264-309) and the "prefetch queue" of PAPER.md:98.            */
-/* Input upload (the e2e path's per-step H2D): copy n_rows x F fp32 rows from
- * pinned, mapped host memory (`host_src`, leading dim ld_src) into device rows
- * `dst` (leading dim ldd) with n_ctas CTAs reading over PCIe and evict-first
- * stores; launch it on a side stream.  Replaces the copy-engine DMA so the
- * concurrent epoch keeps its L2 working set.  F, ld_src, ldd multiples of 4. */
-int cg_upload_rows(int64_t n_rows, int F, const float *host_src, int64_t ld_src, float *dst,
-                   int64_t ldd, int n_ctas, void *stream);
-
 int cg_copy_rows(int64_t n, int F, const int32_t *src_id, const int32_t *src_row,
                  const int32_t *dst_row, const float *const *tab, const int64_t *tab_ld,
                  float *dst, int64_t ld_dst, void *stream);
@@ -143,8 +135,9 @@ int cg_colsum(int64_t M, int N, const float *D, int64_t ldd, float *db, float *w
  * grad2 (optional): also grad[r, c] * scale2[r] (scale2 NULL = 1), the
  * row-scaled gradient the backward aggregation gathers, written in the same
  * pass (the ldg-wide row, padding included).
- * ws: >= n_rows + 1 floats, zeroed by the caller once (the kernel re-arms the
- * finish ticket it keeps there).                                         */
+ * ws: >= n_rows + 1 floats, zeroed by the caller once.  ws[0] is the finish
+ * ticket (fixed offset; each launch re-arms it), ws[1..] the block partials,
+ * so one workspace may be reused across calls of any shape on one stream. */
 int cg_softmax_ce(int64_t n_rows, int C, const float *logits, int64_t ld,
                   const int32_t *label, float inv_n, float *grad, int64_t ldg,
                   float *loss_out, float *ws, float *grad2, int64_t ldg2,

@@ -156,7 +156,7 @@ class TrainSession:
     """
 
     def __init__(self, g, part, profiles, caps, cfg, record_trace: bool = False, *,
-                 model: str = "gcn", num_classes: int = 40, gemm: str = "fp32",
+                 model: str = "gcn", num_classes: int = 40, gemm: str = "3xtf32",
                  plan_mode: str = "auto", keep_logits: str = "last", keep_params: bool = False,
                  timers: bool = True, seed: int = 2, graphs: bool | None = None):
         import torch
@@ -311,7 +311,7 @@ class TrainSession:
 
 
 def train(g, part, profiles, caps, cfg, record_trace: bool = False, *, model: str = "gcn",
-          num_classes: int = 40, gemm: str = "fp32", plan_mode: str = "auto",
+          num_classes: int = 40, gemm: str = "3xtf32", plan_mode: str = "auto",
           keep_logits: str = "last", keep_params: bool = False, timers: bool = True,
           seed: int = 2, on_epoch=None, graphs: bool | None = None) -> TrainReport:
     """Run cfg.epochs real training epochs of the partitioned GNN on B200s.

@@ -14,7 +14,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libcapgnn.so")
-SOURCES = ["abi.cu", "kernels.cu", "spmm_tma.cu", "spmm_async.cu", "gemm.cu", "gemm_tc.cu", "planner.cpp",
+SOURCES = ["abi.cu", "kernels.cu", "spmm_async.cu", "gemm.cu", "gemm_tc.cu", "planner.cpp",
            "graph_host.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

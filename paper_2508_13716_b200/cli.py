@@ -45,53 +45,74 @@ _PROFILE_DEFAULTS = {"out": "devices.json", "n": 16384, "reps": 50, "density": 0
                      "gemm": "3xtf32", "gpus": None}
 
 
-def _as_int_list(value) -> list[int]:
-    if isinstance(value, str):
-        value = [x for x in value.replace(",", " ").split() if x]
-    try:
-        return [int(x) for x in value]
-    except (TypeError, ValueError):
-        raise ParseError(f"expected a list of integers, got {value!r}") from None
-
-
-def _resolve(args, defaults: dict) -> dict:
-    file_cfg = {}
-    if getattr(args, "config", None) is not None:
+def _int_list(value) -> list[int]:
+    """'256,256 256' or [256, 256] -> [256, 256]."""
+    items = value.replace(",", " ").split() if isinstance(value, str) else list(value)
+    out = []
+    for x in items:
         try:
-            with open(args.config, "r", encoding="utf-8") as fh:
-                file_cfg = json.load(fh)
-        except json.JSONDecodeError as exc:
-            raise ParseError(f"{args.config}: invalid JSON: {exc}") from None
-        if not isinstance(file_cfg, dict):
-            raise ParseError(f"{args.config}: config must be a JSON object")
-        unknown = set(file_cfg) - set(defaults)
-        if unknown:
-            raise ParseError(f"{args.config}: unknown keys {sorted(unknown)}")
-    opts = {}
-    for key, default in defaults.items():
-        flag = getattr(args, key, None)
-        opts[key] = flag if flag is not None else file_cfg.get(key, default)
-    return opts
+            out.append(int(x))
+        except (TypeError, ValueError):
+            raise ParseError(f"not an integer list: {value!r}") from None
+    return out
 
 
-def _require(opts, key, flag):
-    if opts[key] is None:
-        raise DomainError(f"{flag} is required (flag or config file)")
+def _read_config(path) -> dict:
+    if path is None:
+        return {}
+    try:
+        doc = json.loads(Path(path).read_text(encoding="utf-8"))
+    except json.JSONDecodeError as exc:
+        raise ParseError(f"{path}: not JSON ({exc})") from None
+    if not isinstance(doc, dict):
+        raise ParseError(f"{path}: the config must be a JSON object")
+    return doc
+
+
+def _options(args, defaults: dict) -> dict:
+    """Layered options, highest first: command-line flags, then the --config
+    file, then the built-in defaults (halopart's precedence, cli.py:92-115).
+    Keys the command does not know are an error."""
+    from collections import ChainMap
+    file_cfg = _read_config(getattr(args, "config", None))
+    extra = sorted(file_cfg.keys() - defaults.keys())
+    if extra:
+        raise ParseError(f"{args.config}: unknown keys {extra}")
+    flags = {k: v for k, v in vars(args).items() if k in defaults and v is not None}
+    return dict(ChainMap(flags, file_cfg, defaults))
+
+
+def _needed(opts: dict, *pairs) -> None:
+    for key, flag in pairs:
+        if opts.get(key) is None:
+            raise DomainError(f"{flag} is required (flag or config file)")
 
 
 def _load_profiles(devices_opt, P: int):
-    if devices_opt is None:   # identical B200 rows (the reference bundles its own fleet)
-        return HG.unit_profiles(P), "builtin:uniform-b200", "-"
-    path = Path(devices_opt)
-    return A.load_device_profiles(path), str(devices_opt), A.sha256_file(path)
+    """--devices, else halopart's bundled fleet (what ``halopart simulate``
+    uses without --devices, cli.py:131-139) when halopart is importable.
+    Without either there is no fleet to size the caches for: error."""
+    if devices_opt is not None:
+        path = Path(devices_opt)
+        return A.load_device_profiles(path), str(devices_opt), A.sha256_file(path)
+    try:
+        from importlib import resources
+        ref = resources.files("halopart.data").joinpath("reference_devices.json")
+        blob = ref.read_bytes()
+    except (ImportError, ModuleNotFoundError, FileNotFoundError):
+        raise DomainError("--devices is required here: halopart (and its bundled "
+                          "reference_devices.json) is not importable") from None
+    import hashlib
+    import io
+    return (A.load_device_profiles(io.StringIO(blob.decode("utf-8"))),
+            "builtin:reference_devices.json", hashlib.sha256(blob).hexdigest())
 
 
 def cmd_train(args) -> int:
     from . import api
-    opts = _resolve(args, _TRAIN_DEFAULTS)
-    _require(opts, "graph", "--graph")
-    _require(opts, "partition_result", "--partition-result")
-    opts["fdim"] = _as_int_list(opts["fdim"])
+    opts = _options(args, _TRAIN_DEFAULTS)
+    _needed(opts, ("graph", "--graph"), ("partition_result", "--partition-result"))
+    opts["fdim"] = _int_list(opts["fdim"])
     graph_path = Path(opts["graph"])
     g = A.load_edge_list(graph_path, compact_ids=bool(opts["compact_ids"]))
     result_path = Path(opts["partition_result"])
@@ -143,8 +164,8 @@ def cmd_train(args) -> int:
 
 def cmd_profile(args) -> int:
     from . import devprofile
-    opts = _resolve(args, _PROFILE_DEFAULTS)
-    gpus = None if opts["gpus"] is None else _as_int_list(opts["gpus"])
+    opts = _options(args, _PROFILE_DEFAULTS)
+    gpus = None if opts["gpus"] is None else _int_list(opts["gpus"])
     rows = devprofile.measure_all(gpus, n=int(opts["n"]), reps=int(opts["reps"]),
                                   density=float(opts["density"]), gemm=str(opts["gemm"]))
     out = Path(opts["out"])

@@ -20,10 +20,6 @@
 #include "pdl.cuh"
 
 extern void cg_set_error(const std::string &msg);
-int cg_spmm_tma(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col,
-                int64_t n_direct, const int32_t *halo_row, const float *X, int64_t ldx,
-                const float *scale, const float *addend, int64_t ld_add, const float *mask,
-                int64_t ld_mask, float *out, int64_t ldo, cudaStream_t st);
 int cg_spmm_async(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col,
                   int64_t n_direct, const int32_t *halo_row, const float *X, int64_t ldx,
                   const float *scale, const float *addend, int64_t ld_add, const float *mask,
@@ -917,53 +913,6 @@ int cg_copy_rows(int64_t n, int F, const int32_t *src_id, const int32_t *src_row
     return 1;
 }
 
-// Input upload by the SMs: rows pulled straight out of pinned (mapped) host
-// memory over PCIe, stored with the streaming (evict-first) hint.  An
-// alternative to the copy engine for the per-step input; measured slower on
-// C2 (its CTAs hold SM slots the persistent epoch kernels wait for), so the
-// engine uses the copy engine unless CG_UPLOAD_CTAS > 0.
-__global__ void k_upload_rows(int64_t n4, int64_t f4, const float4 *__restrict__ src,
-                              int64_t ls4, float4 *__restrict__ dst, int64_t ld4) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    constexpr int U = 8;
-    for (; i + (U - 1) * stride < n4; i += U * stride) {
-        float4 v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t k = i + u * stride, r = k / f4, c = k - r * f4;
-            v[u] = __ldcs(src + r * ls4 + c);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t k = i + u * stride, r = k / f4, c = k - r * f4;
-            __stcs(dst + r * ld4 + c, v[u]);
-        }
-    }
-    for (; i < n4; i += stride) {
-        const int64_t r = i / f4, c = i - r * f4;
-        __stcs(dst + r * ld4 + c, __ldcs(src + r * ls4 + c));
-    }
-}
-
-int cg_upload_rows(int64_t n_rows, int F, const float *host_src, int64_t ld_src, float *dst,
-                   int64_t ldd, int n_ctas, void *stream) {
-    if (n_rows == 0 || F == 0) return 0;
-    if (F % 4 || ld_src % 4 || ldd % 4 || ((uintptr_t)host_src % 16) || ((uintptr_t)dst % 16)) {
-        cg_set_error("cg_upload_rows: F and leading dims must be multiples of 4, 16-B aligned");
-        return -1;
-    }
-    void *dsrc = nullptr;
-    cudaError_t e = cudaHostGetDevicePointer(&dsrc, const_cast<float *>(host_src), 0);
-    if (e != cudaSuccess) return cg_cuda_fail(e, "cg_upload_rows: source is not mapped pinned memory");
-    if (n_ctas <= 0) n_ctas = 16;
-    k_upload_rows<<<n_ctas, 256, 0, (cudaStream_t)stream>>>(
-        n_rows * (F / 4), F / 4, reinterpret_cast<const float4 *>(dsrc), ld_src / 4,
-        reinterpret_cast<float4 *>(dst), ldd / 4);
-    CG_CHECK_LAUNCH("k_upload_rows");
-    return 1;
-}
-
 int cg_spmm(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col, int64_t n_direct,
             const int32_t *halo_row, const float *X, int64_t ldx, const float *scale,
             const float *addend, int64_t ld_add, const float *mask, int64_t ld_mask, float *out,
@@ -1011,12 +960,6 @@ int cg_spmm(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col, in
             total += rc;
         }
         if (total > 0) return total;
-    }
-    static const bool use_tma = getenv("CG_SPMM_TMA") && atoi(getenv("CG_SPMM_TMA")) == 1;
-    if (use_tma) {   // TMA gather4 variant (spmm_tma.cu)
-        const int rc = cg_spmm_tma(n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, scale,
-                                   addend, ld_add, mask, ld_mask, out, ldo, st);
-        if (rc != 0) return rc;
     }
     const int nchunk = F / 4;
     const int threads = 256;
@@ -1096,15 +1039,16 @@ int cg_softmax_ce(int64_t n_rows, int C, const float *logits, int64_t ld, const 
     int blocks;
     if (narrow) {
         blocks = grid_for(n_rows * 4, 256, n_sms() * 8);
-        // ws[0, blocks): block partials; the word after them: the finish ticket
-        // (zero on entry: the caller's zeroed workspace, re-armed by each launch)
-        unsigned int *ticket = reinterpret_cast<unsigned int *>(ws + blocks);
+        // ws[0]: the finish ticket at a fixed offset, so one zeroed workspace
+        // serves calls of any shape (zero on entry, re-armed by each launch);
+        // ws[1, 1 + blocks): block partials
+        unsigned int *ticket = reinterpret_cast<unsigned int *>(ws);
         if (C <= 32)
             cgpdl::launch(k_softmax_ce4<2>, dim3(blocks), dim3(256), 0, st, n_rows, C, logits, ld,
-                          label, inv_n, grad, ldg, ws, grad2, ldg2, scale2, loss_out, ticket);
+                          label, inv_n, grad, ldg, ws + 1, grad2, ldg2, scale2, loss_out, ticket);
         else
             cgpdl::launch(k_softmax_ce4<4>, dim3(blocks), dim3(256), 0, st, n_rows, C, logits, ld,
-                          label, inv_n, grad, ldg, ws, grad2, ldg2, scale2, loss_out, ticket);
+                          label, inv_n, grad, ldg, ws + 1, grad2, ldg2, scale2, loss_out, ticket);
         CG_CHECK_LAUNCH("cg_softmax_ce");
         return 1;
     } else {

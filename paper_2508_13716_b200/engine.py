@@ -22,8 +22,6 @@ from .layout import RunLayout
 from .planner import EpochPlan, SequentialPlanner
 
 GEMM_MODES = {"fp32": 0, "3xtf32": 1, "tf32": 2}
-# CTAs of the SM-driven input upload (cg_upload_rows); 0 = copy-engine DMA (default)
-_UPLOAD_CTAS = int(os.environ.get("CG_UPLOAD_CTAS", "0"))
 
 
 def _dev(a, dtype, device):
@@ -46,7 +44,7 @@ class EpochStats:
 class Engine:
     def __init__(self, layout: RunLayout, me: int, kind: str, dims: list[int], bpe: int,
                  caps, planner: SequentialPlanner, staleness: int, policy: str,
-                 comm=None, lr: float = 0.01, gemm: str = "fp32", params_init=None,
+                 comm=None, lr: float = 0.01, gemm: str = "3xtf32", params_init=None,
                  device: int | None = None, freeze_epoch: int | None = None,
                  record_outcomes: bool = False, plan_mode: str = "auto",
                  graphs: bool | None = None):
@@ -529,7 +527,9 @@ class Engine:
         # the wide last layer's gathered rows G = norm_dst * dL come out of the
         # same pass (no separate scaling launch)
         l = self.nL - 1
-        g2 = ptr(self.Gs[l & 1]) if self._last_wide() else None
+        # (nL == 1: the only backward layer is l = 0, which never reads G --
+        # and G is sized for the hidden widths, not the class width)
+        g2 = ptr(self.Gs[l & 1]) if self._last_wide() and self.nL > 1 else None
         sc = ptr(self.norm_dst) if g2 is not None else None
         call("cg_softmax_ce", self.D.n_in, self.C, ptr(self.logits), self.C4, ptr(self.labels),
              1.0 / self.L.n, ptr(self.dL), self.C4, loss_ptr, ptr(self.ce_ws), g2, self.C4, sc,
@@ -774,16 +774,8 @@ class Engine:
         st = io["h2d"]
         if io["free"] is not None:
             st.wait_event(io["free"])      # the previous upload has been consumed
-        if _UPLOAD_CTAS > 0 and host_x.is_pinned() and host_x.is_contiguous():
-            # SM-driven zero-copy read (cg_upload_rows; CG_UPLOAD_CTAS > 0): an
-            # alternative measured slower -- its CTAs hold SMs the persistent
-            # epoch kernels need
-            call("cg_upload_rows", host_x.shape[0], host_x.shape[1], host_x.data_ptr(),
-                 host_x.shape[1], ptr(io["stage"]), io["stage"].shape[1], _UPLOAD_CTAS,
-                 st.cuda_stream)
-        else:
-            with torch.cuda.stream(st):
-                io["stage"].copy_(host_x, non_blocking=True)
+        with torch.cuda.stream(st):
+            io["stage"].copy_(host_x, non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(st)
         io["ready"] = ev
@@ -797,6 +789,10 @@ class Engine:
         F0 = self.F[0]
         call("cg_scale_rows_to", ptr(self.X[0]), F0, ptr(io["stage"]), F0, self.D.n_in, F0,
              ptr(self.norm_src) if self.kind == "gcn" else None, self.stream())
+        if self.comm.world > 1:
+            # peers read these rows (IPC) in their layer-0 staging / snapshot
+            # copies: every rank's new inputs land before anyone pulls
+            self.comm.barrier()
         ev = torch.cuda.Event()
         ev.record(cs)
         io["free"], io["ready"] = ev, None

@@ -70,12 +70,49 @@ def test_cli_option_precedence(tmp_path):
     cfgf = tmp_path / "c.json"
     cfgf.write_text(json.dumps({"epochs": 7, "policy": "lru"}))
     args = cli.build_parser().parse_args(["train", "--config", str(cfgf), "--policy", "fifo"])
-    opts = cli._resolve(args, cli._TRAIN_DEFAULTS)
+    opts = cli._options(args, cli._TRAIN_DEFAULTS)
     assert opts["epochs"] == 7 and opts["policy"] == "fifo" and opts["staleness"] == -1
     cfgf.write_text(json.dumps({"bogus": 1}))
     with pytest.raises(ParseError):
-        cli._resolve(args, cli._TRAIN_DEFAULTS)
+        cli._options(args, cli._TRAIN_DEFAULTS)
     assert cli.main(["train"]) == 2                      # missing --graph: exit 2
+    assert cli._int_list("128, 256 256") == [128, 256, 256]
+    with pytest.raises(ParseError):
+        cli._int_list("128,x")
+
+
+def test_cli_default_fleet_is_halopart_s():
+    """Without --devices, train uses the fleet `halopart simulate` uses (its
+    bundled reference_devices.json); without halopart it refuses instead of
+    silently sizing caches for another fleet."""
+    import importlib.util
+    if importlib.util.find_spec("halopart") is None:
+        with pytest.raises(DomainError):
+            cli._load_profiles(None, 4)
+    ref_src = "/root/reference/pkg/src"   # build container only
+    if not os.path.isdir(ref_src):
+        pytest.skip("halopart sources not present (GPU box)")
+    code = ("from paper_2508_13716_b200 import cli; p, where, dig = cli._load_profiles(None, 4); "
+            "print(len(p), where, dig, p[0].id, p[0].mem_gb)")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True,
+                       env={**os.environ, "PYTHONPATH": ref_src}, timeout=120)
+    assert r.returncode == 0, r.stderr[-2000:]
+    n, where, dig, pid, mem = r.stdout.split()
+    data = open(os.path.join(ref_src, "halopart", "data", "reference_devices.json"), "rb").read()
+    assert where == "builtin:reference_devices.json"
+    assert dig == hashlib.sha256(data).hexdigest()
+    assert int(n) == len(json.loads(data)) and pid == json.loads(data)[0]["id"]
+
+
+def test_emit_is_all_or_nothing(tmp_path):
+    A.emit(tmp_path / "ok", {"a.txt": b"1", "b.txt": b"2"}, {"tool": "t"})
+    man = json.loads((tmp_path / "ok" / "manifest.json").read_text())
+    assert man["outputs"] == ["a.txt", "b.txt", "manifest.json"]
+    assert sorted(p.name for p in (tmp_path / "ok").iterdir()) == ["a.txt", "b.txt",
+                                                                   "manifest.json"]
+    with pytest.raises(TypeError):
+        A.emit(tmp_path / "bad", {"a.txt": b"1", "b.txt": 5}, {"tool": "t"})
+    assert list((tmp_path / "bad").iterdir()) == []
 
 
 @pytest.mark.gpu

@@ -93,23 +93,6 @@ def test_copy_rows_table():
     assert np.array_equal(dst.cpu().numpy(), exp)
 
 
-@pytest.mark.parametrize("n,F,lds,ldd,ctas", [(169343, 128, 128, 128, 16), (1001, 36, 40, 44, 3),
-                                              (5, 4, 4, 8, 64)])
-def test_upload_rows_from_pinned_host(n, F, lds, ldd, ctas):
-    """cg_upload_rows: SM-driven copy out of pinned host memory, bit-exact,
-    strided on both sides, rows beyond n untouched."""
-    import torch
-    from paper_2508_13716_b200._lib import call, ptr
-    host = torch.from_numpy(np.random.default_rng(n).standard_normal((n, lds)).astype(np.float32))
-    host = host.pin_memory()
-    dst = torch.full((n + 3, ldd), 7.0, device="cuda")
-    call("cg_upload_rows", n, F, host.data_ptr(), lds, ptr(dst), ldd, ctas, _st())
-    _sync()
-    got = dst.cpu().numpy()
-    assert np.array_equal(got[:n, :F], host.numpy()[:, :F])
-    assert (got[:n, F:] == 7.0).all() and (got[n:] == 7.0).all()
-
-
 @pytest.mark.parametrize("shape", [(1000, 40, 256, 0), (777, 256, 128, 0), (513, 64, 36, 1),
                                    (2048, 256, 256, 1)])
 def test_gemm_epilogue(shape):

@@ -2,7 +2,9 @@
 
 Integer parity is exact (per-epoch local/global/miss counts, bytes, trace);
 float parity: per-epoch loss and all-vertex logits within 1e-4 relative
-(fp32 kernels vs the float64 oracle; GEMM mode fp32 SIMT).
+(fp32 kernels vs the float64 oracle).  The GEMMs run train()'s default, the
+tcgen05 3xTF32 kernel, unless a case names the SIMT fp32 opt-in; free-running
+GraphSAGE + 3xTF32 carries the stated looser bound FREE_TOL.
 """
 
 from __future__ import annotations
@@ -23,42 +25,6 @@ def _train(g, ps, caps, cfg, kind, C, **kw):
                      keep_logits="all", **kw)
 
 
-CASES = [
-    # kind, n, deg, P, f_dim, C, capacity ("auto" | int), policy, s, epochs
-    ("gcn", 400, 6.0, 4, (16, 32, 32), 7, "auto", "jaca", -1, 4),
-    ("gcn", 400, 6.0, 4, (16, 32), 5, 0, "jaca", -1, 3),
-    ("gcn", 500, 5.0, 3, (16, 32, 32), 6, 60, "jaca", 1, 5),
-    ("gcn", 500, 5.0, 3, (16, 32, 32), 6, 60, "jaca", 0, 4),
-    ("sage", 400, 6.0, 4, (16, 32, 32), 7, "auto", "jaca", -1, 4),
-    ("sage", 500, 5.0, 3, (16, 32), 6, 60, "fifo", 1, 4),
-    ("gcn", 300, 8.0, 2, (8, 16), 4, 40, "lru", -1, 4),
-]
-
-
-@pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}-P{c[3]}-{c[6]}-{c[7]}-s{c[8]}")
-def test_train_matches_oracle(case):
-    from paper_2508_13716_b200 import hostgraph as H
-    kind, n, deg, P, f_dim, C, cap, policy, s, epochs = case
-    g, ps, og, ops = workload(n, deg, P)
-    if cap == "auto":
-        caps = H.compute_capacities(ps, -1, [180.0] * P, 1024.0, 64.0, 2048.0, f_dim, len(f_dim))
-    else:
-        caps = H.uniform_capacities(ps, cap, f_dim)
-    cfg = H.SimConfig(epochs=epochs, policy=policy, staleness_bound=s, f_dim=f_dim,
-                      L=len(f_dim))
-    rep = _train(g, ps, caps, cfg, kind, C, record_trace=True)
-    pr, outs, _ = oracle_run(og, ops, kind, f_dim, C, caps, policy, s, epochs)
-    # integer parity: counts per (epoch, partition) and the trace
-    for p in pr.plans:
-        got = [(r.local_hits, r.global_hits, r.misses) for r in rep.records if r.epoch == p.epoch]
-        assert got == [tuple(int(x) for x in c) for c in p.counts], p.epoch
-    assert rep.trace_csv == pr.trace_csv(ops.halo)
-    # float parity
-    for e, o in enumerate(outs):
-        assert abs(rep.losses[e] - o.loss) <= TOL * abs(o.loss), (e, rep.losses[e], o.loss)
-        assert rel_err(rep.logits_per_epoch[e], o.logits) <= TOL, e
-
-
 # Free-running trajectories (no weight forcing) through Adam: Adam's first
 # steps are sign-like (m / sqrt(v)), so gradient components near zero turn
 # 1e-6-level product differences into O(lr) weight differences.  fp32 SIMT
@@ -67,6 +33,51 @@ def test_train_matches_oracle(case):
 # bound) is measured at 1.1e-4 .. 1.5e-4 over epochs 2-3 -> stated bound 5e-4.
 FREE_TOL = {("gcn", "fp32"): TOL, ("sage", "fp32"): TOL, ("gcn", "3xtf32"): TOL,
             ("sage", "3xtf32"): 5e-4}
+
+
+CASES = [
+    # kind, n, deg, P, f_dim, C, capacity ("auto" | int), policy, s, epochs, gemm
+    ("gcn", 400, 6.0, 4, (16, 32, 32), 7, "auto", "jaca", -1, 4, "3xtf32"),
+    ("gcn", 400, 6.0, 4, (16, 32), 5, 0, "jaca", -1, 3, "3xtf32"),
+    ("gcn", 500, 5.0, 3, (16, 32, 32), 6, 60, "jaca", 1, 5, "3xtf32"),
+    ("gcn", 500, 5.0, 3, (16, 32, 32), 6, 60, "jaca", 0, 4, "3xtf32"),
+    ("sage", 400, 6.0, 4, (16, 32, 32), 7, "auto", "jaca", -1, 4, "3xtf32"),
+    ("sage", 500, 5.0, 3, (16, 32), 6, 60, "fifo", 1, 4, "3xtf32"),
+    ("gcn", 300, 8.0, 2, (8, 16), 4, 40, "lru", -1, 4, "3xtf32"),
+    # one layer (the logits gradient is never aggregated): narrow and wide C
+    ("gcn", 400, 6.0, 4, (32,), 7, 60, "jaca", 1, 3, "3xtf32"),
+    ("sage", 400, 6.0, 4, (16,), 40, "auto", "jaca", -1, 3, "3xtf32"),
+    # the SIMT fp32 GEMM (explicit opt-in)
+    ("gcn", 500, 5.0, 3, (16, 32, 32), 6, 60, "jaca", 1, 4, "fp32"),
+    ("sage", 400, 6.0, 4, (16, 32, 32), 7, "auto", "jaca", -1, 3, "fp32"),
+]
+
+
+@pytest.mark.parametrize("case", CASES,
+                         ids=lambda c: f"{c[0]}-L{len(c[4])}-P{c[3]}-{c[6]}-{c[7]}-s{c[8]}-{c[10]}")
+def test_train_matches_oracle(case):
+    from paper_2508_13716_b200 import hostgraph as H
+    kind, n, deg, P, f_dim, C, cap, policy, s, epochs, gemm = case
+    g, ps, og, ops = workload(n, deg, P)
+    if cap == "auto":
+        caps = H.compute_capacities(ps, -1, [180.0] * P, 1024.0, 64.0, 2048.0, f_dim, len(f_dim))
+    else:
+        caps = H.uniform_capacities(ps, cap, f_dim)
+    cfg = H.SimConfig(epochs=epochs, policy=policy, staleness_bound=s, f_dim=f_dim,
+                      L=len(f_dim))
+    rep = _train(g, ps, caps, cfg, kind, C, record_trace=True, gemm=gemm)
+    pr, outs, _ = oracle_run(og, ops, kind, f_dim, C, caps, policy, s, epochs)
+    # integer parity: counts per (epoch, partition) and the trace
+    for p in pr.plans:
+        got = [(r.local_hits, r.global_hits, r.misses) for r in rep.records if r.epoch == p.epoch]
+        assert got == [tuple(int(x) for x in c) for c in p.counts], p.epoch
+    assert rep.trace_csv == pr.trace_csv(ops.halo)
+    # float parity: epoch 1 at 1e-4 always, later (free-running) epochs at
+    # the mode's stated bound
+    for e, o in enumerate(outs):
+        tol = TOL if e == 0 else FREE_TOL[(kind, gemm)]
+        assert abs(rep.losses[e] - o.loss) <= tol * abs(o.loss), (e, rep.losses[e], o.loss)
+        assert rel_err(rep.logits_per_epoch[e], o.logits) <= tol, e
 
 
 @pytest.mark.parametrize("kind", ["gcn", "sage"])
