@@ -38,6 +38,10 @@ sys.path.insert(0, ROOT)
 # BASELINE.json configs (C2 is the default bench line; C3 / C4 are extra
 # measurement runs of the larger shapes, selected with --config)
 CONFIGS = {
+    "c1": dict(n=10000, e=200000, f_dim=(128, 128), classes=40, model="gcn", hops=1, parts=4,
+               workload="C1 ER graph 10,000 v / 200,000 e, GCN 2-layer f_dim (128,128) -> 40 "
+                        "classes, P=4 random partitions, JACA Algorithm-1 capacities, "
+                        "staleness -1 (BASELINE.json configs[0], the CPU-runnable case)"),
     "c2": dict(n=169343, e=1166244, f_dim=(128, 256, 256), classes=40, model="gcn", hops=1,
                workload="C2 ogbn-arxiv-shaped ER graph 169,343 v / 1,166,244 e, GCN 3-layer "
                         "f_dim (128,256,256) -> 40 classes, P=8 random partitions, JACA "
@@ -59,10 +63,21 @@ CONFIG = "c2"
 
 
 def apply_config(name: str) -> None:
-    global N_C2, E_C2, F_DIM, CLASSES, MODEL, HOPS, WORKLOAD, CONFIG
+    global N_C2, E_C2, F_DIM, CLASSES, MODEL, HOPS, WORKLOAD, CONFIG, PARTS
     c = CONFIGS[name]
     N_C2, E_C2, F_DIM, CLASSES = c["n"], c["e"], c["f_dim"], c["classes"]
     MODEL, HOPS, WORKLOAD, CONFIG = c["model"], c["hops"], c["workload"], name
+    PARTS = c.get("parts", 8)
+
+
+def mapped_repo_libs() -> list[str]:
+    """Shared objects from this repo mapped into this process."""
+    try:
+        with open("/proc/self/maps") as fh:
+            paths = {ln.split()[-1] for ln in fh if ln.rstrip().endswith(".so")}
+    except OSError:
+        return []
+    return sorted(os.path.relpath(p, ROOT) for p in paths if p.startswith(ROOT + os.sep))
 
 
 def peaks():
@@ -283,6 +298,10 @@ def run_ours(args):
                    "kind": "port", "sample": "not run: one oracle-port epoch of this shape "
                    "exceeds the bench's few-minute budget (see the C2 line)"}
     sess.close()
+    del sess, eng
+    exchange = None
+    if CONFIG == "c2" and not args.no_exchange:
+        exchange = exchange_record(args, g, ps, world)
     if rank == 0:
         line = {
             "metric": "full-batch epoch GTEPS (L*|E|/epoch time)",
@@ -328,60 +347,222 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
+            "exchange": exchange,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-class OracleSession:
-    """The CPU oracle port of the same workload, stepped one epoch at a time
-    (plan: pure-Python CacheSystem restatement; model: float64 numpy/scipy)."""
+def sum_over_ranks(x, world: int, backend: str):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(np.asarray(x, np.float64), device="cuda" if backend == "nccl" else "cpu")
+    dist.all_reduce(t)
+    return t.cpu().numpy()
 
-    def __init__(self, g, ps, caps, staleness: int = -1):
+
+def pcie_peaks(nbytes: int = 256 << 20):
+    """Copy-engine H2D / D2H GB/s of one pinned buffer (best of 5)."""
+    import torch
+    h = torch.empty(nbytes // 4, dtype=torch.float32).pin_memory()
+    d = torch.empty_like(h, device="cuda")
+    out = {}
+    for name, (dst, src) in (("h2d", (d, h)), ("d2h", (h, d))):
+        best = 1e9
+        for _ in range(5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            dst.copy_(src, non_blocking=True)
+            b.record()
+            torch.cuda.synchronize()
+            best = min(best, a.elapsed_time(b))
+        out[name] = nbytes / (best / 1e3) / 1e9
+    return out
+
+
+EXCHANGE_CAP, EXCHANGE_S = 40000, 1
+
+
+def exchange_record(args, g, ps, world: int, epochs: int = 8):
+    """The exchange path, timed: C2 with uniform capacity 40,000 per cache
+    level and staleness 1 (the reference-golden case ``u40000_s1``), so every
+    epoch has misses, stale global hits served from the pinned host tier,
+    local-slab write-through and host-tier write-through.  Per epoch: device
+    time, each K3 launch class's CUDA-event time, and the rows each class
+    moved by tier (read from that epoch's plan tables), as wire bytes next to
+    the reference's model bytes (simulator.py:232-236)."""
+    import torch
+    from paper_2508_13716_b200 import api, hostgraph as H
+    caps = H.uniform_capacities(ps, EXCHANGE_CAP, F_DIM)
+    cfg = H.SimConfig(epochs=args.warmup + epochs, policy="jaca", staleness_bound=EXCHANGE_S,
+                      f_dim=F_DIM, L=len(F_DIM))
+    sess = api.TrainSession(g, ps, H.unit_profiles(ps.P), caps, cfg, model=MODEL,
+                            num_classes=CLASSES, gemm=args.gemm, keep_logits="none")
+    eng = sess.engine
+    eng.k3_timing(True)
+    for _ in range(args.warmup):
+        sess.step()
+    classes = ("stage", "write_through", "write_back", "grad_pull", "snapshot")
+    tiers = ("stage_host", "stage_peer", "stage_hbm", "write_through", "write_back",
+             "grad_pull")
+    width = eng.k3_widths()
+    ep_s, k3_ms, rows, counts = [], [], [], []
+    for _ in range(epochs):
+        st = sess.step()                    # synchronous: events read per epoch
+        ep_s.append(st.seconds)
+        k3_ms.append([st.k3.get(c, 0.0) if st.k3 else 0.0 for c in classes])
+        r = eng.k3_rows()
+        rows.append([r[t] for t in tiers])
+        counts.append(np.asarray(st.counts).sum(0))
+    sess.close()
+    ep = max_over_ranks(float(np.mean(ep_s)), world, args.dist_backend)
+    k3 = np.asarray(k3_ms).mean(0)
+    k3 = [max_over_ranks(float(x), world, args.dist_backend) for x in k3]
+    rows_tot = sum_over_ranks(np.asarray(rows, np.float64).mean(0), world, args.dist_backend)
+    wire = {t: float(rows_tot[i]) * width[t] * 4 for i, t in enumerate(tiers)}
+    cnt = np.asarray(counts).mean(0)     # every rank plans every partition: no sum
+    bpe = caps.bytes_per_entry
+    pcie = pcie_peaks()
+    k3d = dict(zip(classes, k3))
+    hbm_peak, _ = peaks()
+
+    def rate(nbytes, ms):
+        return nbytes / (ms / 1e3) / 1e9 if ms > 0 else None
+    stage_bytes = wire["stage_host"] + wire["stage_peer"] + wire["stage_hbm"]
+    return {
+        "workload": f"C2, uniform capacity {EXCHANGE_CAP} per level (c_gpu, c_cpu), staleness "
+                    f"{EXCHANGE_S}, JACA (reference golden u40000_s1); epochs "
+                    f"{args.warmup + 1}..{args.warmup + epochs} (K6-planned, period-2 plan)",
+        "ms_per_epoch": ep * 1e3, "gteps": len(F_DIM) * g.n_edges / ep / 1e9,
+        "lookups_per_epoch": {"local_hits": float(cnt[0]), "global_hits": float(cnt[1]),
+                              "misses": float(cnt[2])},
+        "model_bytes_per_epoch": {"fwd_cached": float(cnt[2]) * bpe,
+                                  "fwd_uncached": float(sum(h.size for h in ps.halo)) * bpe,
+                                  "bwd": float(sum(ps.cut_edges)) * bpe},
+        "wire_bytes_per_epoch": {"pcie_read (global-tier hits, pinned host -> HBM)":
+                                     wire["stage_host"],
+                                 "pcie_write (global-tier write-through, HBM -> pinned host)":
+                                     wire["write_through"],
+                                 "nvlink (peer pulls: misses + backward gradient rows)":
+                                     wire["stage_peer"] + wire["grad_pull"],
+                                 "hbm (local-slab fills and write-back)":
+                                     wire["stage_hbm"] + wire["write_back"]},
+        "rows_per_epoch": {t: float(rows_tot[i]) for i, t in enumerate(tiers)},
+        "k3_ms_per_epoch": k3d,
+        "k3_share_of_epoch": sum(k3) / (ep * 1e3),
+        "k3_GB_s": {"stage": rate(stage_bytes, k3d["stage"]),
+                    "write_through": rate(wire["write_through"], k3d["write_through"]),
+                    "write_back": rate(wire["write_back"], k3d["write_back"]),
+                    "grad_pull": rate(wire["grad_pull"], k3d["grad_pull"])},
+        "peaks_GB_s": {"pcie_h2d_dma": pcie["h2d"], "pcie_d2h_dma": pcie["d2h"],
+                       "hbm": hbm_peak, "nvlink_per_direction": 900.0},
+        "note": "N=1: all 8 partitions share the GPU, so a miss reads the co-resident owner's "
+                "row in place inside the SpMM gather (no K3 row, no wire byte) unless the "
+                "vertex is locally cached (then it is written through into the slab, HBM); "
+                "NVLink rows appear only at N>1",
+    }
+
+
+class OracleSession:
+    """The CPU path of the same workload, one epoch per ``step()``: the
+    planner port (pure-Python restatement of halopart's ``simulator.run``
+    lookup loop, simulator.py:206-226) plus the PyTorch-CPU fp32 epoch
+    (oracle/torch_port.py, all host cores) -- BASELINE.md §4's CPU baseline.
+    Built from oracle-side graph objects only; nothing of the product."""
+
+    def __init__(self, og, ops, caps, staleness: int = -1, threads: int | None = None):
         from oracle import halo_port as ohp
         from oracle import model_port as omp
-        og = ohp.GraphCSR(n=g.n_vertices, n_edges=g.n_edges, out_off=g.out_offsets,
-                          out_tgt=g.out_targets, in_off=g.in_offsets, in_tgt=g.in_targets)
-        opart = ohp.Partitions(n=g.n_vertices, P=ps.P, parts=None, inner=ps.inner,
-                               halo=ps.halo, hops=1, overlap=ps.overlap_count,
-                               cut=ps.cut_edges, all_edges=ps.all_edges)
-        v, _, _, sc = ohp.influence(og, opart)
-        ranked = ohp.ranked_halos(opart, v, sc)
+        from oracle import torch_port as otp
+        v, _, _, sc = ohp.influence(og, ops)
+        ranked = ohp.ranked_halos(ops, v, sc)
         imp = {int(a): float(b) for a, b in zip(v, sc)}
         dims = list(F_DIM) + [CLASSES]
-        self.planner = ohp.Planner("jaca", (caps.c_cpu, tuple(caps.c_gpu),
-                                            caps.bytes_per_entry), ranked, ps.halo, imp)
-        self.trainer = omp.Trainer(og, ps.inner, ps.halo, omp.ModelSpec(MODEL, dims),
-                                   omp.features(g.n_vertices, F_DIM[0], 0),
-                                   omp.labels(g.n_vertices, CLASSES, 1),
-                                   params=omp.init_params(MODEL, dims, 2))
+        self.planner = ohp.Planner("jaca", caps, ranked, ops.halo, imp)
+        self.threads = threads or len(os.sched_getaffinity(0))
+        self.trainer = otp.TorchTrainer(og, ops.inner, ops.halo, omp.ModelSpec(MODEL, dims),
+                                        omp.features(og.n, F_DIM[0], 0),
+                                        omp.labels(og.n, CLASSES, 1),
+                                        params=omp.init_params(MODEL, dims, 2),
+                                        threads=self.threads)
+        self._live = otp.live_versions
         self.s = staleness
         self.e = 0
-        self.n_edges = g.n_edges
+        self.plan_s, self.train_s = [], []
 
-    def step(self) -> float:
-        t0 = time.perf_counter()
+    def step(self):
         self.e += 1
+        t0 = time.perf_counter()
         plan = self.planner.step(self.e, self.s)
-        self.trainer.step(plan.version)
-        return time.perf_counter() - t0
+        t1 = time.perf_counter()
+        out = self.trainer.step(plan.version, self._live(self.planner.cache)
+                                if self.e % 4 == 0 else None)
+        t2 = time.perf_counter()
+        self.plan_s.append(t1 - t0)
+        self.train_s.append(t2 - t1)
+        return t2 - t0, plan, out
 
 
-def cpu_baseline(g, ps, caps, budget_s: float = 20.0):
-    """Oracle port timed on the host cores over a bounded sample (>= 2 epochs)."""
-    sess = OracleSession(g, ps, caps)
+def oracle_inputs(g=None, ps=None, caps=None, parts: int | None = None):
+    """Oracle-side (graph, partitions, capacities): converted from the
+    product's host objects when given, else built by the oracle itself (the
+    reference arm must not map the product library)."""
+    from oracle import halo_port as ohp
+    parts = parts or PARTS
+    if g is None:
+        og = ohp.er_graph(N_C2, E_C2 / N_C2, 0)
+        ops = ohp.partition_set(og, ohp.random_assignment(N_C2, parts, 0), HOPS)
+        c = ohp.capacities_auto(ops, -1, [180.0] * parts, 1024.0, 64.0, 2048.0, F_DIM)
+        return og, ops, (c[0], tuple(c[1]), c[2])
+    og = ohp.GraphCSR(n=g.n_vertices, n_edges=g.n_edges, out_off=g.out_offsets,
+                      out_tgt=g.out_targets, in_off=g.in_offsets, in_tgt=g.in_targets)
+    ops = ohp.Partitions(n=g.n_vertices, P=ps.P, parts=None, inner=ps.inner, halo=ps.halo,
+                         hops=HOPS, overlap=ps.overlap_count, cut=ps.cut_edges,
+                         all_edges=ps.all_edges)
+    return og, ops, (caps.c_cpu, tuple(caps.c_gpu), caps.bytes_per_entry)
+
+
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def time_cpu_path(sess: OracleSession, warmup: int, steps: int, budget_s: float):
+    """Warm-up epochs, then timed epochs (at least one) within the budget."""
+    t_start = time.perf_counter()
+    for _ in range(warmup):
+        sess.step()
     times = []
-    t_all = time.perf_counter()
-    while len(times) < 2 or (time.perf_counter() - t_all < budget_s and len(times) < 4):
-        times.append(sess.step())
-    per_epoch = statistics.mean(times[1:])   # epoch 1 includes the warm fill
-    return {"value": len(F_DIM) * g.n_edges / per_epoch / 1e9, "unit": "GTEPS",
-            "cores": len(os.sched_getaffinity(0)), "kind": "port",
-            "sample": f"{len(times)} epochs of the same C2 workload through the oracle port "
-                      f"(pure-Python cache plan + float64 numpy/scipy model), first epoch "
-                      f"excluded; mean {per_epoch:.2f} s/epoch",
-            "seconds_per_epoch": per_epoch}
+    while len(times) < steps:
+        times.append(sess.step()[0])
+        if time.perf_counter() - t_start > budget_s:
+            break
+    k = len(times)
+    return statistics.mean(times), statistics.mean(sess.plan_s[-k:]), statistics.mean(sess.train_s[-k:]), k
+
+
+def cpu_baseline(g, ps, caps, budget_s: float = 30.0):
+    """The CPU path on the host cores over a bounded sample: 1 warm-up epoch
+    (it holds the epoch-1 snapshot build), then epochs until the budget."""
+    og, ops, ocaps = oracle_inputs(g, ps, caps)
+    sess = OracleSession(og, ops, ocaps)
+    per, plan_s, train_s, k = time_cpu_path(sess, 1, 3, budget_s)
+    return {"value": len(F_DIM) * g.n_edges / per / 1e9, "unit": "GTEPS",
+            "cores": sess.threads, "kind": "port",
+            "sample": f"{k} timed epoch(s) after 1 warm-up of the same {CONFIG.upper()} workload: "
+                      f"planner port (pure Python, 1 core) {plan_s:.2f} s + PyTorch-CPU fp32 "
+                      f"epoch ({sess.threads} threads) {train_s:.2f} s per epoch",
+            "seconds_per_epoch": per, "plan_s": plan_s, "train_s": train_s,
+            "cpu": _cpu_model()}
 
 
 def run_reference(args):
@@ -389,32 +570,38 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    g, ps, caps = build_workload(args.parts)
-    sess = OracleSession(g, ps, caps, args.staleness)
-    t_start = time.perf_counter()
-    times = []
-    for i in range(args.warmup + args.steps):
-        times.append(sess.step())
-        # bound the whole run to a few minutes: keep >= 1 timed epoch
-        if time.perf_counter() - t_start > args.ref_budget and len(times) > min(args.warmup, 1):
-            break
-    timed = times[min(args.warmup, len(times) - 1):]
-    per_epoch = statistics.mean(timed)
-    value = len(F_DIM) * g.n_edges / per_epoch / 1e9
-    sample = (f"{len(timed)} timed epoch(s) after {len(times) - len(timed)} warm-up of the C2 "
-              f"workload through the oracle port (pure-Python cache plan + float64 "
-              f"numpy/scipy model); budget {args.ref_budget:.0f} s")
+    og, ops, caps = oracle_inputs(parts=args.parts)
+    sess = OracleSession(og, ops, caps, args.staleness)
+    per, plan_s, train_s, k = time_cpu_path(sess, args.warmup, args.steps, args.ref_budget)
+    value = len(F_DIM) * og.n_edges / per / 1e9
+    sample = (f"{k} timed epoch(s) after {args.warmup} warm-up of the {CONFIG.upper()} workload "
+              f"(budget {args.ref_budget:.0f} s): planner port (pure Python, 1 core) "
+              f"{plan_s:.2f} s + PyTorch-CPU fp32 epoch ({sess.threads} threads) {train_s:.2f} s")
     line = {"impl": "reference", "metric": "full-batch epoch GTEPS (L*|E|/epoch time)",
-            "value": value, "unit": "GTEPS", "n_gpus": world, "steps": len(timed),
-            "warmup": len(times) - len(timed), "ms_per_step": per_epoch * 1e3,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "value": value, "unit": "GTEPS", "n_gpus": world, "steps": k,
+            "warmup": args.warmup, "ms_per_step": per * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": {"workload": WORKLOAD, "partitions": args.parts},
-            "cpu_baseline": {"value": value, "unit": "GTEPS",
-                             "cores": len(os.sched_getaffinity(0)), "kind": "port",
-                             "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": sess.threads,
+                             "kind": "port", "sample": sample, "cpu": _cpu_model(),
+                             "plan_s": plan_s, "train_s": train_s},
             "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            "repo_libs_mapped": mapped_repo_libs()}
     print(json.dumps(line), flush=True)
+
+
+def self_launch(args) -> int:
+    """``--gpus N`` without a launcher: re-run this script under
+    torch.distributed.run with N ranks on 127.0.0.1."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -423,7 +610,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--parts", type=int, default=PARTS)
+    ap.add_argument("--parts", type=int, default=None)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--e2e-logits", action="store_true",
                     help="e2e: also download the logits every step")
@@ -431,13 +618,19 @@ def main():
                     help=argparse.SUPPRESS)
     ap.add_argument("--staleness", type=int, default=-1)
     ap.add_argument("--gemm", default="3xtf32", choices=["fp32", "3xtf32", "tf32"])
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--cpu-budget", type=float, default=30.0)
     ap.add_argument("--ref-budget", type=float, default=150.0)
+    ap.add_argument("--no-exchange", action="store_true",
+                    help="skip the exchange-path record (C2 only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     apply_config(args.config)
+    if args.parts is None:
+        args.parts = PARTS
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        sys.exit(self_launch(args))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -39,6 +39,7 @@ class EpochStats:
     planner: str                 # "host" or "gpu"
     flag: int = 0
     events: tuple | None = None  # (t0, t1) CUDA events when not yet synchronised
+    k3: list | dict | None = None  # K3 launches: [(class, ev0, ev1)] -> {class: ms}
 
 
 class Engine:
@@ -80,7 +81,23 @@ class Engine:
         self.use_graphs = bool(graphs) and isinstance(self.comm, SoloComm)
         self._capturing = False
         self._graphs = None
+        # K3 launch timing (bench exchange record): pre-made event pairs,
+        # handed out in launch order each epoch; see k3_timing()
+        self._k3_pool, self._k3_used = None, None
         self._alloc(caps, params_init)
+
+    def k3_timing(self, on: bool = True, pool: int = 64) -> None:
+        """Time every K3 launch (halo staging, write-through, write-back,
+        snapshot fill, backward gradient pulls) with CUDA events on the
+        launching stream; EpochStats.k3 then maps each class to its ms."""
+        if on and self._k3_pool is None:
+            self._k3_pool = [(torch.cuda.Event(enable_timing=True),
+                              torch.cuda.Event(enable_timing=True)) for _ in range(pool)]
+            for a, b in self._k3_pool:   # materialise before any graph capture
+                a.record()
+                b.record()
+        self._k3_on = bool(on)
+        self._graphs = None   # re-capture with (or without) the event nodes
 
     # ------------------------------------------------------------------ setup
     def _alloc(self, caps, params_init):
@@ -453,9 +470,18 @@ class Engine:
         return "host", plan.counts.copy(), plan
 
     # ------------------------------------------------------------------ epoch
-    def _copy(self, n, F, src_id, src_row, dst_row, tab, tab_ld, dst, ld):
+    _k3_on = False
+
+    def _copy(self, n, F, src_id, src_row, dst_row, tab, tab_ld, dst, ld, cls="stage"):
+        ev = None
+        if self._k3_on and self._k3_used is not None and len(self._k3_used) < len(self._k3_pool):
+            ev = self._k3_pool[len(self._k3_used)]
+            self._k3_used.append((cls, F, ev))
+            self._rec(ev[0])
         call("cg_copy_rows", n, F, ptr(src_id), ptr(src_row), ptr(dst_row), ptr(tab),
              ptr(tab_ld), dst if isinstance(dst, int) else ptr(dst), ld, self.stream())
+        if ev is not None:
+            self._rec(ev[1])
 
     def _gw(self, l: int):
         # compact layout: every read is a version-0 local hit (enforced by the
@@ -466,7 +492,7 @@ class Engine:
         F = self.F[l]
         self._copy(self.L.union.size, F, self.gw_src_id, self.gw_src_row, self.gw_slot,
                    self.tab[l], self.tab_ld[l], self.host.ptr + 4 * int(self.layer_off[l]),
-                   self.bpe_f)
+                   self.bpe_f, cls="write_through")
 
     def _rec(self, ev) -> None:
         """Record a timing event on the current stream; inside a capture it
@@ -486,7 +512,7 @@ class Engine:
             if e == 1 and D.n_snap:
                 # epoch-1 snapshot of every halo vertex read on this device
                 self._copy(D.n_snap, F, self.snap_src, self.snap_srow, self.snap_dst,
-                           self.tab[l], self.tab_ld[l], self.X[l], F)
+                           self.tab[l], self.tab_ld[l], self.X[l], F, cls="snapshot")
             if D.n_halo and not self.L.compact:   # compact: nothing is ever staged
                 self._copy(D.n_halo, F, self.stage_src, self.stage_row, self.stage_dst,
                            self.tab[l], self.tab_ld[l], self.X[l], F)
@@ -498,7 +524,8 @@ class Engine:
                 self._rec(spmm_ev[l][1])
             if self.wb is not None:
                 sid, srow, dst, n = self.wb
-                self._copy(n, F, sid, srow, dst, self.tab[l], self.tab_ld[l], self.X[l], F)
+                self._copy(n, F, sid, srow, dst, self.tab[l], self.tab_ld[l], self.X[l], F,
+                           cls="write_back")
             last = l == nL - 1
             out = self.logits if last else self.X[l + 1]
             if last and not self._capturing:
@@ -576,7 +603,7 @@ class Engine:
             self.comm.barrier()
             if self.n_bwd:
                 self._copy(self.n_bwd, Fx, self.b_src, self.b_row, self.b_dst, self.tabGs[l & 1],
-                           self._tabG_ld(Fx), G, Fx)
+                           self._tabG_ld(Fx), G, Fx, cls="grad_pull")
             k = nL - 1 - l
             if spmm_ev is not None:
                 self._rec(spmm_ev[k][0])
@@ -642,6 +669,7 @@ class Engine:
         # launches recorded by the capture run on each replay, not now
         before = dict(_lib.launches)
         self._capturing = True
+        self._k3_used = [] if self._k3_on else None
         try:
             with torch.cuda.graph(g1, pool=pool):
                 self.plan(e)
@@ -655,12 +683,13 @@ class Engine:
         recorded = {k: v - before.get(k, 0) for k, v in _lib.launches.items()
                     if v != before.get(k, 0)}
         _lib.count_replay({k: -v for k, v in recorded.items()})
-        self._graphs = (g1, g2, fwd_ev, bwd_ev, recorded)
+        self._graphs = (g1, g2, fwd_ev, bwd_ev, recorded, self._k3_used)
+        self._k3_used = None
 
     def _run_epoch_graph(self, e: int, timers: bool, sync: bool) -> EpochStats:
         if self._graphs is None:
             self._capture(e)
-        g1, g2, fwd_ev, bwd_ev, recorded = self._graphs
+        g1, g2, fwd_ev, bwd_ev, recorded, k3_used = self._graphs
         cs = torch.cuda.current_stream(self.dev)
         t0 = t1 = None
         if timers:
@@ -689,6 +718,7 @@ class Engine:
         stats.counts = self.k6["counts"].clone()
         stats.flag = self.k6["flag"].clone()
         stats.loss = self.grads[self.n_params:].clone()
+        stats.k3 = list(k3_used) if (timers and k3_used) else None
         return self.finish(stats) if sync else stats
 
     def run_epoch(self, e: int, timers: bool = True, sync: bool = True) -> EpochStats:
@@ -700,6 +730,7 @@ class Engine:
             t0.record()
         fwd_ev = self._new_timers(self.nL) if timers else None
         bwd_ev = self._new_timers(self.nL - 1) if timers else None
+        self._k3_used = [] if (timers and self._k3_on) else None
         self._mark("plan")
         mode, hcounts, _ = self.plan(e)
         self._consume_input()
@@ -722,7 +753,8 @@ class Engine:
         self._mark(None)
         stats = EpochStats(epoch=e, loss=float("nan"), counts=hcounts, seconds=0.0,
                            spmm_fwd_ms=fwd_ev or [], spmm_bwd_ms=bwd_ev or [], planner=mode,
-                           events=(t0, t1) if timers else None)
+                           events=(t0, t1) if timers else None, k3=self._k3_used)
+        self._k3_used = None
         if mode == "gpu":
             # keep this epoch's counters on the device until finish()
             stats.counts = self.k6["counts"].clone()
@@ -751,6 +783,11 @@ class Engine:
             stats.spmm_fwd_ms = [a.elapsed_time(b) for a, b in stats.spmm_fwd_ms]
             stats.spmm_bwd_ms = [a.elapsed_time(b) for a, b in stats.spmm_bwd_ms]
             stats.events = None
+        if isinstance(stats.k3, list):
+            k3 = {}
+            for cls, F, (a, b) in stats.k3:
+                k3[cls] = k3.get(cls, 0.0) + a.elapsed_time(b)
+            stats.k3 = k3
         return stats
 
     # ------------------------------------------------------------ host I/O
@@ -829,6 +866,37 @@ class Engine:
         if self.kind == "gcn":
             call("cg_scale_rows", ptr(self.X[0]), self.F[0], D.n_in, self.F[0],
                  ptr(self.norm_src), self.stream())
+
+    def k3_rows(self) -> dict:
+        """Rows the K3 launches of the epoch just run move, by class and tier,
+        read from this epoch's device tables (a sync; keep it outside timed
+        regions).  Tiers: ``host`` = pinned global tier over PCIe, ``peer`` =
+        another GPU over NVLink, ``hbm`` = this GPU."""
+        D, nd, me = self.D, self.L.n_dev, self.me
+        out = {"stage_host": 0, "stage_peer": 0, "stage_hbm": 0, "write_through": 0,
+               "write_back": 0, "grad_pull": int(self.n_bwd)}
+        if D.n_halo and not self.L.compact:
+            src, dst = self.stage_src[:D.n_halo], self.stage_dst[:D.n_halo]
+            live = (src >= 0) & (dst >= 0)
+            out["stage_host"] = int((live & (src == nd)).sum())
+            out["stage_peer"] = int((live & (src != nd) & (src != me)).sum())
+            out["stage_hbm"] = int((live & (src == me)).sum())
+        if (self.c_cpu and self.L.union is not None and self.L.union.size
+                and not self.L.compact):
+            out["write_through"] = int((self.gw_slot >= 0).sum())
+        if self.wb is not None:
+            out["write_back"] = int(self.wb[3])
+        return out
+
+    def k3_widths(self) -> dict:
+        """Floats per row each K3 class moves per epoch, summed over the
+        layers it runs in (stage / write-through / write-back: every layer's
+        input width; gradient pulls: the hidden layers' aggregated width)."""
+        fsum = int(sum(self.F))
+        widths = list(self.F) + [self.C4]
+        gsum = int(sum(min(widths[l], widths[l + 1]) for l in range(1, self.nL)))
+        return {"stage_host": fsum, "stage_peer": fsum, "stage_hbm": fsum,
+                "write_through": fsum, "write_back": fsum, "grad_pull": gsum}
 
     def gpu_outcomes(self) -> np.ndarray:
         """Per-requester outcomes of the last GPU-planned epoch (flat order)."""

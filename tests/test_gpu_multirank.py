@@ -119,7 +119,8 @@ def test_bench_two_ranks_one_gpu():
     port = _free_port()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", f"--master-port={port}", "bench.py", "--gpus", "2",
-           "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--dist-backend", "gloo"]
+           "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--dist-backend", "gloo",
+           "--no-exchange"]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
@@ -127,3 +128,24 @@ def test_bench_two_ranks_one_gpu():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["partitions_per_gpu"] == 4
     assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+
+
+def test_bench_self_launches_gpus_n():
+    """`bench.py --gpus 2` with no launcher re-runs itself under
+    torch.distributed.run (2 ranks on 127.0.0.1) and reports n_gpus 2, with
+    the exchange record summed / maxed over the ranks."""
+    import json
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    cmd = [sys.executable, "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3",
+           "--no-cpu-baseline", "--dist-backend", "gloo"]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["partitions_per_gpu"] == 4
+    ex = d["exchange"]
+    assert ex["lookups_per_epoch"]["misses"] > 0 and ex["k3_ms_per_epoch"]["stage"] > 0
+    nv = [v for k, v in ex["wire_bytes_per_epoch"].items() if k.startswith("nvlink")][0]
+    assert nv > 0          # two ranks: misses and gradient rows cross devices (IPC)

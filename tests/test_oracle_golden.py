@@ -106,3 +106,29 @@ def test_c2_config_setup_parity():
     cfg = load_json("c2.json")
     n = 169343
     _config_setup(cfg, n, 1166244 / n, 8)
+
+
+@pytest.mark.parametrize("kind,s,cap", [("gcn", 1, 60), ("sage", -1, None), ("gcn", 0, 30),
+                                        ("sage", 1, 40)])
+def test_torch_port_matches_model_port(kind, s, cap):
+    """The PyTorch-CPU fp32 epoch (the timed CPU baseline)
+    computes model_port's float64 epochs within 1e-5 (measured ~1e-6)."""
+    from oracle import model_port as omp
+    from oracle import torch_port as otp
+    n, P, f_dim, C = 400, 4, (16, 32, 32), 7
+    g = hp.er_graph(n, 6.0, 0)
+    ps = hp.partition_set(g, hp.random_assignment(n, P, 0), 1)
+    verts, _, _, score = hp.influence(g, ps)
+    imp = {int(v): float(x) for v, x in zip(verts, score)}
+    caps = hp.capacities_uniform(ps, cap if cap is not None else 10 ** 6, f_dim)
+    pl = hp.Planner("jaca", caps, hp.ranked_halos(ps, verts, score), ps.halo, imp)
+    dims = list(f_dim) + [C]
+    spec = omp.ModelSpec(kind, dims)
+    X, y = omp.features(n, f_dim[0], 0), omp.labels(n, C, 1)
+    a = omp.Trainer(g, ps.inner, ps.halo, spec, X, y, params=omp.init_params(kind, dims, 2))
+    b = otp.TorchTrainer(g, ps.inner, ps.halo, spec, X, y, params=omp.init_params(kind, dims, 2))
+    for e in range(1, 6):
+        plan = pl.step(e, s)
+        oa, ob = a.step(plan.version), b.step(plan.version, otp.live_versions(pl.cache))
+        assert np.abs(oa.logits - ob.logits).max() <= 1e-5 * np.abs(oa.logits).max(), e
+        assert abs(oa.loss - ob.loss) <= 1e-5 * oa.loss, e
