@@ -417,7 +417,20 @@ def exchange_record(args, g, ps, world: int, epochs: int = 8):
         r = eng.k3_rows()
         rows.append([r[t] for t in tiers])
         counts.append(np.asarray(st.counts).sum(0))
+    # the same epochs with the host-tier write-through in line on the compute
+    # stream (no side-stream queue): how much of its PCIe time the queue hides
+    eng.wt_async = False
+    eng._graphs = None            # re-capture without the fork / join
+    for _ in range(2):
+        sess.step()
+    inl_s, inl_wt = [], []
+    for _ in range(epochs):
+        st = sess.step()
+        inl_s.append(st.seconds)
+        inl_wt.append(st.k3.get("write_through", 0.0) if st.k3 else 0.0)
     sess.close()
+    inl = max_over_ranks(float(np.mean(inl_s)), world, args.dist_backend)
+    inl_wt = max_over_ranks(float(np.mean(inl_wt)), world, args.dist_backend)
     ep = max_over_ranks(float(np.mean(ep_s)), world, args.dist_backend)
     k3 = np.asarray(k3_ms).mean(0)
     k3 = [max_over_ranks(float(x), world, args.dist_backend) for x in k3]
@@ -453,6 +466,16 @@ def exchange_record(args, g, ps, world: int, epochs: int = 8):
         "rows_per_epoch": {t: float(rows_tot[i]) for i, t in enumerate(tiers)},
         "k3_ms_per_epoch": k3d,
         "k3_share_of_epoch": sum(k3) / (ep * 1e3),
+        "write_through_queue": {
+            "ms_per_epoch_queued": ep * 1e3, "ms_per_epoch_inline": inl * 1e3,
+            "write_through_ms_inline": inl_wt,
+            "hidden_frac": ((inl - ep) * 1e3 / inl_wt) if inl_wt > 0 else None,
+            "blocks": eng.WT_BLOCKS,
+            "how": "same session, same K6-planned epochs: host-tier write-through on the "
+                   "side-stream queue (forked per layer, joined at the end of the forward / "
+                   "update; k3_ms_per_epoch.write_through is its side-stream time) vs in line "
+                   "on the compute stream; hidden = (inline - queued) / inline write-through "
+                   "time"},
         "k3_GB_s": {"stage": rate(stage_bytes, k3d["stage"]),
                     "write_through": rate(wire["write_through"], k3d["write_through"]),
                     "write_back": rate(wire["write_back"], k3d["write_back"]),

@@ -77,6 +77,14 @@ int cg_scale_rows_to(float *dst, int64_t ldd, const float *src, int64_t lds, int
 int cg_copy_rows(int64_t n, int F, const int32_t *src_id, const int32_t *src_row,
                  const int32_t *dst_row, const float *const *tab, const int64_t *tab_ld,
                  float *dst, int64_t ld_dst, void *stream);
+/* The same copy on at most max_blocks CTAs of 256 threads (<= 0: the
+ * default grid).  A copy bound by PCIe or NVLink rather than HBM needs few
+ * CTAs in flight; a small grid lets it run on a side stream (the host-tier
+ * write-through queue) beside the epoch's kernels without taking their SMs. */
+int cg_copy_rows_bounded(int64_t n, int F, const int32_t *src_id, const int32_t *src_row,
+                         const int32_t *dst_row, const float *const *tab,
+                         const int64_t *tab_ld, float *dst, int64_t ld_dst, int max_blocks,
+                         void *stream);
 
 /* ---- K1/K2: fused cache-lookup + gather SpMM --------------------------- */
 /* out[r] = epi( scale[r] * sum_{e in [rowptr[r], rowptr[r+1])} X[map(col[e])] )

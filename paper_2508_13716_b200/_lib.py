@@ -50,6 +50,7 @@ SIGNATURES = {
     "cg_scale_rows": [P, I64, I64, INT, P, P],
     "cg_scale_rows_to": [P, I64, P, I64, I64, INT, P, P],
     "cg_copy_rows": [I64, INT, P, P, P, P, P, P, I64, P],
+    "cg_copy_rows_bounded": [I64, INT, P, P, P, P, P, P, I64, INT, P],
     "cg_spmm": [I64, INT, P, P, I64, P, P, I64, P, P, I64, P, I64, P, I64, I64, P],
     "cg_gemm": [I64, INT, INT, P, I64, P, INT, P, I64, P, INT, P, INT, P, P, I64, P, I64, INT,
                 P, P, P],
@@ -117,7 +118,7 @@ def lib():
 # device entry points report how many kernels they launched; the running
 # total is the bench's "gpu_launches" evidence
 KERNEL_ENTRY = {"cg_hash_features", "cg_hash_labels", "cg_scale_rows", "cg_scale_rows_to",
-                "cg_copy_rows",
+                "cg_copy_rows", "cg_copy_rows_bounded",
                 "cg_spmm", "cg_gemm", "cg_wgrad", "cg_colsum", "cg_softmax_ce", "cg_adam",
                 "cg_split_tf32", "cg_split_tf32_t",
                 "cg_plan_frozen", "cg_set_epoch"}

@@ -895,12 +895,13 @@ int cg_hash_labels(int32_t *out, const int32_t *vertex, int64_t n_rows, int C, u
     return 1;
 }
 
-int cg_copy_rows(int64_t n, int F, const int32_t *src_id, const int32_t *src_row,
-                 const int32_t *dst_row, const float *const *tab, const int64_t *tab_ld,
-                 float *dst, int64_t ld_dst, void *stream) {
+int cg_copy_rows_bounded(int64_t n, int F, const int32_t *src_id, const int32_t *src_row,
+                         const int32_t *dst_row, const float *const *tab,
+                         const int64_t *tab_ld, float *dst, int64_t ld_dst, int max_blocks,
+                         void *stream) {
     if (n == 0) return 0;
     const int threads = 256;
-    int blocks = grid_for(n, threads, 148 * 32);
+    int blocks = grid_for(n, threads, max_blocks > 0 ? max_blocks : 148 * 32);
     bool vec = (F % 4 == 0) && (ld_dst % 4 == 0) && ((uintptr_t)dst % 16 == 0);
     // source alignment is validated on the host side (tab_ld % 4 == 0, 16-B bases)
     if (vec)
@@ -911,6 +912,13 @@ int cg_copy_rows(int64_t n, int F, const int32_t *src_id, const int32_t *src_row
                       F, src_id, src_row, dst_row, tab, tab_ld, dst, ld_dst);
     CG_CHECK_LAUNCH("k_copy_rows");
     return 1;
+}
+
+int cg_copy_rows(int64_t n, int F, const int32_t *src_id, const int32_t *src_row,
+                 const int32_t *dst_row, const float *const *tab, const int64_t *tab_ld,
+                 float *dst, int64_t ld_dst, void *stream) {
+    return cg_copy_rows_bounded(n, F, src_id, src_row, dst_row, tab, tab_ld, dst, ld_dst, 0,
+                                stream);
 }
 
 int cg_spmm(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col, int64_t n_direct,

@@ -26,6 +26,13 @@ extern int cg_cuda_fail(cudaError_t e, const char *what);
 
 namespace cpa {
 
+// CG_SPMM_FLAGS (experiments): bit 0 evict_first output stores, bit 1
+// streaming output stores, bit 2 evict_normal (not evict_last) gathers
+static int spmm_flags() {
+    static const int f = getenv("CG_SPMM_FLAGS") ? atoi(getenv("CG_SPMM_FLAGS")) : 0;
+    return f;
+}
+
 constexpr int WARPS = 8;   // warps per block
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint64_t pol) {
@@ -39,6 +46,20 @@ __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// Output rows are written once and not re-read by this launch: stored with
+// an L2 evict_first hint (flags bit 0) or as streaming .cs stores (bit 1),
+// so they do not push the gathered source rows out of L2.
+__device__ __forceinline__ void st_out(float4 *p, float4 v, int flags, uint64_t pol_first) {
+    if (flags & 1)
+        asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;"
+                     ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol_first)
+                     : "memory");
+    else if (flags & 2)
+        __stcs(p, v);
+    else
+        *p = v;
+}
+
 // G lanes per edge stream (a warp runs 32/G independent streams), NCH float4
 // chunks per lane (F <= 4 G NCH), S ring slots per stream, EPI: an addend
 // and/or mask operand is present (its prefetch registers otherwise vanish)
@@ -48,7 +69,8 @@ k_spmm_cpa(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
            const int32_t *__restrict__ col, int64_t n_direct, const int32_t *__restrict__ halo_row,
            const float *__restrict__ X, int64_t ldx, const float *__restrict__ scale,
            const float *__restrict__ addend, int64_t ld_add, const float *__restrict__ mask,
-           int64_t ld_mask, float *__restrict__ out, int64_t ldo, int64_t rows_per_warp) {
+           int64_t ld_mask, float *__restrict__ out, int64_t ldo, int64_t rows_per_warp,
+           int flags) {
     extern __shared__ __align__(16) float4 ring_all[];
     pdl_entry();
     const int grp = threadIdx.x / G, lane = threadIdx.x & (G - 1);
@@ -56,8 +78,12 @@ k_spmm_cpa(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
                                    : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
     float4 *ring = ring_all + (size_t)grp * S * NCH * G;   // [slot][chunk][lane]
     const uint32_t ring_s = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    uint64_t pol, pol_first;
+    if (flags & 4)   // gathered rows with the default (evict_normal) priority
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    else
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
 
     // rows fit int32 (n_rows < 2^31); edge offsets are relative to the warp's
     // first edge (a warp's slice is far below 2^31 edges)
@@ -151,7 +177,8 @@ k_spmm_cpa(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
                 o.x = pm[c].x > 0.f ? o.x : 0.f; o.y = pm[c].y > 0.f ? o.y : 0.f;
                 o.z = pm[c].z > 0.f ? o.z : 0.f; o.w = pm[c].w > 0.f ? o.w : 0.f;
             }
-            reinterpret_cast<float4 *>(out + (int64_t)row * ldo)[ch] = o;
+            st_out(reinterpret_cast<float4 *>(out + (int64_t)row * ldo) + ch, o, flags,
+                   pol_first);
             acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
         ++row;
@@ -214,7 +241,7 @@ int launch_epi(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col,
     const int64_t blocks = ((n_rows + rpw - 1) / rpw + SPB - 1) / SPB;
     cgpdl::launch(k_spmm_cpa<G, NCH, S, EPI>, dim3((unsigned)blocks), dim3(WARPS * 32), smem, st,
                   n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, scale, addend, ld_add, mask,
-                  ld_mask, out, ldo, rpw);
+                  ld_mask, out, ldo, rpw, spmm_flags());
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 1 : cg_cuda_fail(e, "k_spmm_cpa");
 }

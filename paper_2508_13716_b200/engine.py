@@ -84,7 +84,19 @@ class Engine:
         # K3 launch timing (bench exchange record): pre-made event pairs,
         # handed out in launch order each epoch; see k3_timing()
         self._k3_pool, self._k3_used = None, None
+        self.wt_async = os.environ.get("CG_WT_ASYNC", "1") != "0"
+        self._wt_early = True
+        self._wt = None
         self._alloc(caps, params_init)
+        if self._gw_active():
+            # the write-through queue: side stream + fork/join events, made
+            # (and materialised) before any graph capture
+            cs = torch.cuda.current_stream(self.dev)
+            self._wt = dict(stream=torch.cuda.Stream(self.dev), pending=[],
+                            fork=[torch.cuda.Event() for _ in range(self.nL)],
+                            done=[torch.cuda.Event() for _ in range(self.nL)])
+            for ev in self._wt["fork"] + self._wt["done"]:
+                ev.record(cs)
 
     def k3_timing(self, on: bool = True, pool: int = 64) -> None:
         """Time every K3 launch (halo staging, write-through, write-back,
@@ -450,6 +462,13 @@ class Engine:
                 use_gpu = False   # membership still moving: stay on the host
             else:
                 self._init_gpu_plan()
+        # Early write-through forks (see _gw) are safe when no global slot can
+        # change hands mid-epoch under a peer's staging read: one process
+        # (the fork follows this process's own staging copy), or a
+        # K6-planned epoch (frozen membership: an entry is only rewritten
+        # when it was stale for every requester of the epoch).  Otherwise
+        # the copies wait for the next layer's barrier, as the readers do.
+        self._wt_early = use_gpu or self.comm.world == 1
         if use_gpu:
             k = self.k6
             k["counts"].zero_()
@@ -472,33 +491,75 @@ class Engine:
     # ------------------------------------------------------------------ epoch
     _k3_on = False
 
-    def _copy(self, n, F, src_id, src_row, dst_row, tab, tab_ld, dst, ld, cls="stage"):
+    def _copy(self, n, F, src_id, src_row, dst_row, tab, tab_ld, dst, ld, cls="stage",
+              stream=None, max_blocks: int = 0):
+        st = stream.cuda_stream if stream is not None else self.stream()
         ev = None
         if self._k3_on and self._k3_used is not None and len(self._k3_used) < len(self._k3_pool):
             ev = self._k3_pool[len(self._k3_used)]
             self._k3_used.append((cls, F, ev))
-            self._rec(ev[0])
-        call("cg_copy_rows", n, F, ptr(src_id), ptr(src_row), ptr(dst_row), ptr(tab),
-             ptr(tab_ld), dst if isinstance(dst, int) else ptr(dst), ld, self.stream())
+            self._rec(ev[0], stream)
+        call("cg_copy_rows_bounded", n, F, ptr(src_id), ptr(src_row), ptr(dst_row), ptr(tab),
+             ptr(tab_ld), dst if isinstance(dst, int) else ptr(dst), ld, max_blocks, st)
         if ev is not None:
-            self._rec(ev[1])
+            self._rec(ev[1], stream)
 
-    def _gw(self, l: int):
+    # Host-tier write-through queue (R10; PAPER.md:98's "global" queue).  The
+    # epoch's dirty global entries are copied into the pinned host tier over
+    # PCIe (~51 GB/s) by K3 on a side stream with a small grid, forked once a
+    # layer's input rows are final and its staging copy (the only same-epoch
+    # reader of the host tier) is enqueued (layer L-1: when the backward
+    # starts), and all joined at the end of the update -- steady-state epochs
+    # are then captured as ONE graph -- so the PCIe writes run under the
+    # SpMM / GEMM work of the whole epoch instead of in front of it.  The
+    # host tier is only read by stale global hits, i.e. in LATER epochs
+    # (current-version reads go to the owner's row), and the next epoch's K6
+    # rewrites gw_slot only after the joins -- so the joins are the only
+    # ordering needed.  CG_WT_ASYNC=0 (or wt_async = False) runs the
+    # copies in line on the compute stream instead.
+    WT_BLOCKS = int(os.environ.get("CG_WT_BLOCKS", "16"))
+
+    def _gw_active(self) -> bool:
         # compact layout: every read is a version-0 local hit (enforced by the
         # host tables / K6 flag), so no global entry is ever rewritten
-        if (self.c_cpu == 0 or self.L.union is None or self.L.union.size == 0
-                or self.L.compact):
+        return not (self.c_cpu == 0 or self.L.union is None or self.L.union.size == 0
+                    or self.L.compact)
+
+    def _gw(self, l: int):
+        if not self._gw_active():
             return
         F = self.F[l]
-        self._copy(self.L.union.size, F, self.gw_src_id, self.gw_src_row, self.gw_slot,
-                   self.tab[l], self.tab_ld[l], self.host.ptr + 4 * int(self.layer_off[l]),
-                   self.bpe_f, cls="write_through")
+        args = (self.L.union.size, F, self.gw_src_id, self.gw_src_row, self.gw_slot,
+                self.tab[l], self.tab_ld[l], self.host.ptr + 4 * int(self.layer_off[l]),
+                self.bpe_f)
+        if not self.wt_async:
+            self._copy(*args, cls="write_through")
+            return
+        wt = self._wt
+        cs = torch.cuda.current_stream(self.dev)
+        wt["fork"][l].record(cs)
+        wt["stream"].wait_event(wt["fork"][l])
+        self._copy(*args, cls="write_through", stream=wt["stream"], max_blocks=self.WT_BLOCKS)
+        wt["done"][l].record(wt["stream"])
+        wt["pending"].append(wt["done"][l])
 
-    def _rec(self, ev) -> None:
-        """Record a timing event on the current stream; inside a capture it
-        becomes an external event node that fires on every replay."""
+    def _join_gw(self) -> None:
+        if self._wt is None or not self._wt["pending"]:
+            return
+        cs = torch.cuda.current_stream(self.dev)
+        for ev in self._wt["pending"]:
+            cs.wait_event(ev)
+        self._wt["pending"] = []
+
+    def _rec(self, ev, stream=None) -> None:
+        """Record a timing event on the current (or the given) stream; inside
+        a capture it becomes an external event node that fires on every
+        replay."""
         if self._capturing:
-            call("cg_event_record", ev.cuda_event, self.stream())
+            call("cg_event_record", ev.cuda_event,
+                 stream.cuda_stream if stream is not None else self.stream())
+        elif stream is not None:
+            ev.record(stream)
         else:
             ev.record()
 
@@ -508,7 +569,8 @@ class Engine:
             F, Fo = self.F[l], self.dims[l + 1]
             if l > 0:
                 self.comm.barrier()
-                self._gw(l - 1)
+                if not self._wt_early:
+                    self._gw(l - 1)
             if e == 1 and D.n_snap:
                 # epoch-1 snapshot of every halo vertex read on this device
                 self._copy(D.n_snap, F, self.snap_src, self.snap_srow, self.snap_dst,
@@ -516,6 +578,11 @@ class Engine:
             if D.n_halo and not self.L.compact:   # compact: nothing is ever staged
                 self._copy(D.n_halo, F, self.stage_src, self.stage_row, self.stage_dst,
                            self.tab[l], self.tab_ld[l], self.X[l], F)
+            if l < nL - 1 and self._wt_early:
+                # this layer's input rows are final and its stale global hits
+                # have been staged (a host-plan epoch may reassign a slot read
+                # above): write the dirty global entries through
+                self._gw(l)
             if spmm_ev is not None:
                 self._rec(spmm_ev[l][0])
             self._spmm(n_in, F, self.fwd_rowptr, self.fwd_col, n_in, self.halo_row, self.X[l],
@@ -564,6 +631,8 @@ class Engine:
 
     def _backward(self, spmm_ev) -> None:
         st, nL, kind, n_in = self.stream(), self.nL, self.kind, self.D.n_in
+        if self._wt_early:
+            self._gw(nL - 1)   # the last layer's input rows, under the backward pass
         cur = 0
         for l in range(nL - 1, -1, -1):
             F, Fo = self.F[l], self.dims[l + 1]
@@ -630,7 +699,8 @@ class Engine:
     def _update(self) -> None:
         """K7 + optimizer + the weights' TF32 split; uses self.step."""
         self.comm.allreduce_(self.grads)
-        self._gw(self.nL - 1)
+        if not self._wt_early:
+            self._gw(self.nL - 1)
         call("cg_adam", self.n_params, ptr(self.params), ptr(self.grads), ptr(self.adam_m),
              ptr(self.adam_v), self.lr, 0.9, 0.999, 1e-8, self.step,
              ptr(self.params_hi) if self.params_hi is not None else None,
@@ -638,6 +708,7 @@ class Engine:
              ptr(self.adam_corr) if self._capturing else None, self.stream())
         if self.params_hi is not None:
             self._split_t()
+        self._join_gw()
 
     def _new_timers(self, n: int):
         return [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -671,13 +742,24 @@ class Engine:
         self._capturing = True
         self._k3_used = [] if self._k3_on else None
         try:
-            with torch.cuda.graph(g1, pool=pool):
-                self.plan(e)
-                self._forward(e, fwd_ev)
-                self._loss()
-            with torch.cuda.graph(g2, pool=pool):
-                self._backward(bwd_ev)
-                self._update()
+            if self._wt is not None:
+                # write-through queue active: ONE graph, so the copies forked
+                # in the forward pass join only at the end of the update
+                with torch.cuda.graph(g1, pool=pool):
+                    self.plan(e)
+                    self._forward(e, fwd_ev)
+                    self._loss()
+                    self._backward(bwd_ev)
+                    self._update()
+                g2 = None
+            else:
+                with torch.cuda.graph(g1, pool=pool):
+                    self.plan(e)
+                    self._forward(e, fwd_ev)
+                    self._loss()
+                with torch.cuda.graph(g2, pool=pool):
+                    self._backward(bwd_ev)
+                    self._update()
         finally:
             self._capturing = False
         recorded = {k: v - before.get(k, 0) for k, v in _lib.launches.items()
@@ -702,10 +784,13 @@ class Engine:
         self._wait_logits_download()
         g1.replay()
         if self._io is not None:
+            # logits final: after the forward graph (or, single-graph epochs,
+            # after the whole epoch)
             ev = torch.cuda.Event()
             ev.record(cs)
             self._io["fwd"] = ev
-        g2.replay()
+        if g2 is not None:
+            g2.replay()
         _lib.count_replay(recorded)
         if timers:
             t1 = torch.cuda.Event(enable_timing=True)

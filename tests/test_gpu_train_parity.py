@@ -189,38 +189,74 @@ def test_rapa_pruned_partition_matches_oracle():
         assert rel_err(rep.logits_per_epoch[e], o.logits) <= TOL, e
 
 
-def test_c2_bench_config_float_parity():
-    """The bench workload itself (C2: 169,343 v / 1,166,244 e, GCN 3-layer
-    128-256-256 -> 40, P = 8 on one GPU, Algorithm-1 capacities, s = -1,
-    3xTF32), full size, 3 epochs vs the float64 oracle:
+# Free-running logits at the C2 size after Adam steps (stated looser bound;
+# the drift grows with the number of Adam steps): measured 2.3e-5 / 3.8e-4
+# (fp32 SIMT) and 8.8e-4 / 2.3e-3 (3xTF32) at epochs 2 / 3 of auto_sneg
+# (tests/diag_c2_parity.py), 6.1e-3 at epoch 4 of u40000_s1
+C2_FREE_LOGITS_TOL = 1.5e-2
+
+
+@pytest.mark.parametrize("cache", ["auto_sneg", "u40000_s1"])
+def test_c2_float_parity(cache):
+    """The bench workload (C2: 169,343 v / 1,166,244 e, GCN 3-layer
+    128-256-256 -> 40, P = 8 on one GPU, 3xTF32 tcgen05 GEMMs), full size,
+    vs the float64 oracle, on both cache configurations the bench times:
+    ``auto_sneg`` (Algorithm-1 capacities, s = -1: the compact layout, every
+    read a version-0 hit) and ``u40000_s1`` (uniform capacity 40,000 per
+    level, s = 1: the exchange path -- misses, stale global hits from the
+    pinned host tier, slab and host write-through):
       * cache counts of every (epoch, partition) exactly;
       * per-epoch arithmetic (oracle restarted from the GPU's weights each
-        epoch) within 1e-5 on all logits and the loss (measured 4e-6);
-      * free-running: the loss within 1e-4 every epoch (measured 1e-7) and
-        the logits of epoch 1 within 1e-4.  Later free-running logits leave
-        1e-4 even for the fp32 SIMT path (2e-5 at epoch 2, 4e-4 at epoch 3,
-        tests/diag_c2_parity.py): Adam's first steps are sign-like, so fp32-
-        vs-float64 gradient differences on near-zero components become
-        O(lr) weight differences -- DESIGN.md section 2."""
+        epoch) within 1e-5 on all logits and the loss;
+      * free-running: the loss within 1e-4 every epoch, the logits of epoch 1
+        within 1e-4, later logits within the stated looser bound
+        C2_FREE_LOGITS_TOL (Adam's first steps are sign-like, so fp32-vs-
+        float64 gradient differences on near-zero components become O(lr)
+        weight differences -- no fp32 implementation holds the float64
+        trajectory to 1e-4 there)."""
     import bench
     from paper_2508_13716_b200 import hostgraph as H
     bench.apply_config("c2")
     g, ps, caps = bench.build_workload(8)
-    cfg = H.SimConfig(epochs=3, policy="jaca", staleness_bound=-1, f_dim=bench.F_DIM, L=3)
+    s, epochs = -1, 3
+    if cache == "u40000_s1":
+        caps, s, epochs = H.uniform_capacities(ps, 40000, bench.F_DIM), 1, 4
+    cfg = H.SimConfig(epochs=epochs, policy="jaca", staleness_bound=s, f_dim=bench.F_DIM, L=3)
     rep = _train(g, ps, caps, cfg, "gcn", bench.CLASSES, gemm="3xtf32", keep_params=True)
-    free = bench.OracleSession(g, ps, caps, -1)
-    forced = bench.OracleSession(g, ps, caps, -1)
-    for e in range(3):
-        free.e += 1
-        forced.e += 1
-        plan = free.planner.step(free.e, -1)
-        forced.planner.step(forced.e, -1)
-        out = free.trainer.step(plan.version)
-        fo = forced.trainer.step(plan.version, forced_params=rep.params_per_epoch[e])
+    og, ops, _ = bench.oracle_inputs(g, ps, caps)
+    pr, forced = oracle_run_forced(og, ops, "gcn", bench.F_DIM, bench.CLASSES, caps, "jaca", s,
+                                   rep.params_per_epoch)
+    for e, (p, fo) in enumerate(zip(pr.plans, forced)):
         got = [(r.local_hits, r.global_hits, r.misses) for r in rep.records if r.epoch == e + 1]
-        assert got == [tuple(int(x) for x in c) for c in plan.counts], e
+        assert got == [tuple(int(x) for x in c) for c in p.counts], e
         assert abs(rep.losses[e] - fo.loss) <= 1e-5 * abs(fo.loss), e
         assert rel_err(rep.logits_per_epoch[e], fo.logits) <= 1e-5, e
+    if cache == "u40000_s1":   # the exchange path really ran
+        assert sum(r.global_hits for r in rep.records) > 0
+        assert sum(r.misses for r in rep.records if r.epoch > 1) > 0
+    _, free, _ = oracle_run(og, ops, "gcn", bench.F_DIM, bench.CLASSES, caps, "jaca", s, epochs)
+    for e, out in enumerate(free):
         assert abs(rep.losses[e] - out.loss) <= TOL * abs(out.loss), (e, rep.losses[e], out.loss)
-        if e == 0:
-            assert rel_err(rep.logits_per_epoch[e], out.logits) <= TOL
+        tol = TOL if e == 0 else C2_FREE_LOGITS_TOL
+        assert rel_err(rep.logits_per_epoch[e], out.logits) <= tol, e
+
+
+def test_write_through_queue_matches_inline(monkeypatch):
+    """The host-tier write-through on its side-stream queue (default) gives
+    bit-identical epochs to the in-line copies, across host-planned and
+    K6-planned (graph-replayed) epochs of a capacity-limited s = 1 run with
+    global-tier hits."""
+    from paper_2508_13716_b200 import hostgraph as H
+    g, ps, _, _ = workload(800, 6.0, 4)
+    f_dim = (16, 32, 32)
+    caps = H.uniform_capacities(ps, 120, f_dim)
+    cfg = H.SimConfig(epochs=7, policy="jaca", staleness_bound=1, f_dim=f_dim, L=3)
+    runs = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("CG_WT_ASYNC", flag)
+        runs.append(_train(g, ps, caps, cfg, "gcn", 6))
+    a, b = runs
+    assert sum(r.global_hits for r in a.records) > 0
+    assert a.losses == b.losses
+    for x, y in zip(a.logits_per_epoch, b.logits_per_epoch):
+        assert np.array_equal(x, y)
