@@ -472,10 +472,10 @@ def exchange_record(args, g, ps, world: int, epochs: int = 8):
             "hidden_frac": ((inl - ep) * 1e3 / inl_wt) if inl_wt > 0 else None,
             "blocks": eng.WT_BLOCKS,
             "how": "same session, same K6-planned epochs: host-tier write-through on the "
-                   "side-stream queue (forked per layer, joined at the end of the forward / "
-                   "update; k3_ms_per_epoch.write_through is its side-stream time) vs in line "
-                   "on the compute stream; hidden = (inline - queued) / inline write-through "
-                   "time"},
+                   "side-stream queue (forked per layer once its rows are final, all joined at "
+                   "the end of the update; one graph per epoch; k3_ms_per_epoch.write_through "
+                   "is its side-stream time) vs in line on the compute stream; hidden = "
+                   "(inline - queued) / inline write-through time"},
         "k3_GB_s": {"stage": rate(stage_bytes, k3d["stage"]),
                     "write_through": rate(wire["write_through"], k3d["write_through"]),
                     "write_back": rate(wire["write_back"], k3d["write_back"]),

@@ -84,9 +84,11 @@ class SampledGraph:
 
 
 def _agg(rows, r, idx, w, H):
-    out = np.zeros((rows.size, H.shape[1]))
-    np.add.at(out, r, w[:, None] * H[idx])
-    return out
+    """sum_e w_e H[idx_e] into row r_e, as one sparse x dense product (no
+    per-edge temporaries: C3's receptive fields hold ~10^7 edges)."""
+    import scipy.sparse as sp
+    A = sp.csr_matrix((w, (r, idx)), shape=(rows.size, H.shape[0]))
+    return np.asarray(A @ H)
 
 
 def sampled_logits(sg: SampledGraph, dims, params_by_epoch, samples: np.ndarray,

@@ -138,6 +138,152 @@ def _model_times(ps, sigma, nrm, cfg):
     return mix, comp
 
 
+def _epoch_records(ps, cfg, mix, comp, bpe, e, counts, tot, out) -> float:
+    """One epoch's per-device records from its cache counts, with the
+    reference's cost model and accounting (simulator.py:226-246); appends to
+    ``out``, accumulates ``tot`` and returns the epoch makespan."""
+    dts = []
+    for i in range(ps.P):
+        lh, gh, ms = (int(x) for x in counts[i])
+        tot += (lh, gh, ms)
+        c = (ms + ps.cut_edges[i]) * mix[i] * cfg.unit_time
+        ov = min(1.0, cfg.prefetch_depth / max(1, len(ps.halo[i])))
+        resid = c - min(c, comp[i]) * ov
+        dt = comp[i] + resid
+        dts.append(dt)
+        out.append(EpochDeviceRecord(
+            epoch=e, device=i, fwd_bytes=ms * bpe, bwd_bytes=ps.cut_edges[i] * bpe,
+            local_hits=lh, global_hits=gh, misses=ms, compute_time=comp[i],
+            comm_time=c, residual_comm_time=resid, device_time=dt))
+    return max(dts)
+
+
+def _validate(part, profiles, caps, cfg):
+    """run()'s argument checks and DomainErrors (simulator.py:174-184)."""
+    ps, sigma = _resolve(part)
+    nrm = _normalize(profiles)
+    if len(caps.c_gpu) != ps.P:
+        raise DomainError(f"capacities cover {len(caps.c_gpu)} devices, partition has {ps.P}")
+    if any(d >= len(nrm) for d in sigma):
+        raise DomainError("sigma names a device outside the profile list")
+    bpe = HG.feature_bytes(cfg.f_dim)
+    if bpe != caps.bytes_per_entry:
+        raise DomainError(
+            f"capacities sized for {caps.bytes_per_entry} B entries, config implies {bpe} B")
+    return ps, sigma, nrm, bpe
+
+
+def _ranked_planner(g, ps, caps, cfg) -> SequentialPlanner:
+    """Importance ranking + warm (simulator.py:186-196), native and bit-exact."""
+    union, score = HG.influence_scores(g, ps)
+    ranked = [h[np.lexsort((h, -score[np.searchsorted(union, h)]))] for h in ps.halo]
+    planner = SequentialPlanner(cfg.policy, caps.c_cpu, caps.c_gpu, union, score,
+                                [np.asarray(h, np.int64) for h in ps.halo], ranked)
+    planner.warm()
+    return planner
+
+
+def simulate(g, part, profiles, caps, cfg, record_trace: bool = False) -> TrainReport:
+    """The cache plan alone, on the host: halopart's ``run()`` (simulator.py:
+    160-256) through the native planner (csrc/planner.cpp), no GPU and no
+    training.  Returns a ``TrainReport`` whose SimReport fields (records,
+    cost-model times, totals, trace) serialise byte-identically to the
+    reference's; the measured fields stay empty.  This is what the policy /
+    capacity sweeps run, at native speed (the reference's per-lookup Python
+    loop takes ~2-4 us per lookup)."""
+    ps, sigma, nrm, bpe = _validate(part, profiles, caps, cfg)
+    planner = _ranked_planner(g, ps, caps, cfg)
+    mix, comp = _model_times(ps, sigma, nrm, cfg)
+    records, spans, rows = [], [], []
+    tot = np.zeros(3, np.int64)
+    for e in range(1, cfg.epochs + 1):
+        plan = planner.epoch(e, cfg.staleness_bound)
+        spans.append(_epoch_records(ps, cfg, mix, comp, bpe, e, plan.counts, tot, records))
+        if record_trace:
+            rows += _trace_rows(planner, e, None)
+    look = int(tot.sum())
+    return TrainReport(
+        config=cfg.to_dict(), sigma=sigma, records=records, epoch_makespans=spans,
+        total_time=sum(spans), total_fwd_bytes=sum(r.fwd_bytes for r in records),
+        total_bwd_bytes=sum(r.bwd_bytes for r in records),
+        hit_rate_local=int(tot[0]) / look if look else 0.0,
+        hit_rate_global=int(tot[1]) / look if look else 0.0,
+        trace_csv=trace_csv(rows) if record_trace else None,
+        n_edges=int(g.n_edges), n_layers=len(cfg.f_dim))
+
+
+def _with_policy(cfg, policy: str):
+    import dataclasses
+    if dataclasses.is_dataclass(cfg):
+        return dataclasses.replace(cfg, policy=policy)
+    return HG.SimConfig(**{**cfg.to_dict(), "policy": policy})
+
+
+def sweep_capacity(g, part, profiles, cfg, capacities, *, train_epochs: bool = False,
+                   **train_kw) -> list:
+    """halopart's ``sweep_capacity`` (simulator.py:259-268): one run per
+    capacity, both cache levels set to it (demand-capped,
+    ``uniform_capacities``).  Plan-only (``simulate``) by default;
+    ``train_epochs=True`` runs real GPU epochs (``train``) per capacity."""
+    if not capacities:
+        raise DomainError("need at least one capacity")
+    ps, _ = _resolve(part)
+    fn = (lambda c: train(g, part, profiles, c, cfg, **train_kw)) if train_epochs else \
+        (lambda c: simulate(g, part, profiles, c, cfg))
+    return [fn(HG.uniform_capacities(ps, int(c), cfg.f_dim)) for c in capacities]
+
+
+@dataclass(frozen=True)
+class ComparisonRow:
+    policy: str
+    capacity: int
+    hit_rate_local: float
+    hit_rate_global: float
+    fwd_bytes: int
+    bwd_bytes: int
+    makespan: float
+
+
+@dataclass
+class ComparisonTable:
+    """Policy x capacity grid (simulator.py:271-297); ``makespan`` is the
+    run's total modelled time."""
+
+    rows: list
+
+    def to_csv(self) -> str:
+        buf = io.StringIO()
+        w = csv.writer(buf, lineterminator="\n")
+        w.writerow(["policy", "capacity", "hit_rate_local", "hit_rate_global", "fwd_bytes",
+                    "bwd_bytes", "makespan"])
+        for r in self.rows:
+            w.writerow([r.policy, r.capacity, r.hit_rate_local, r.hit_rate_global,
+                        r.fwd_bytes, r.bwd_bytes, r.makespan])
+        return buf.getvalue()
+
+
+def compare_policies(g, part, profiles, cfg, policies=("jaca", "fifo", "lru"),
+                     capacities=(0,), *, train_epochs: bool = False,
+                     **train_kw) -> ComparisonTable:
+    """halopart's ``compare_policies`` (simulator.py:300-322): the identical
+    workload under each policy and capacity (plan-only by default, real GPU
+    epochs with ``train_epochs=True``)."""
+    ps, _ = _resolve(part)
+    rows = []
+    for policy in policies:
+        pcfg = _with_policy(cfg, policy)
+        for c in capacities:
+            caps = HG.uniform_capacities(ps, int(c), cfg.f_dim)
+            rep = (train(g, part, profiles, caps, pcfg, **train_kw) if train_epochs
+                   else simulate(g, part, profiles, caps, pcfg))
+            rows.append(ComparisonRow(policy=policy, capacity=int(c),
+                                      hit_rate_local=rep.hit_rate_local,
+                                      hit_rate_global=rep.hit_rate_global,
+                                      fwd_bytes=rep.total_fwd_bytes,
+                                      bwd_bytes=rep.total_bwd_bytes, makespan=rep.total_time))
+    return ComparisonTable(rows=rows)
+
+
 class TrainSession:
     """The drop-in's stepwise form: ``train()``'s setup once, then one real
     training epoch per ``step()``.
@@ -165,17 +311,7 @@ class TrainSession:
 
         if not torch.cuda.is_available():
             raise RuntimeError("train() needs a CUDA device: the hot path has no CPU fallback")
-        ps, sigma = _resolve(part)
-        P = ps.P
-        nrm = _normalize(profiles)
-        if len(caps.c_gpu) != P:
-            raise DomainError(f"capacities cover {len(caps.c_gpu)} devices, partition has {P}")
-        if any(d >= len(nrm) for d in sigma):
-            raise DomainError("sigma names a device outside the profile list")
-        bpe = HG.feature_bytes(cfg.f_dim)
-        if bpe != caps.bytes_per_entry:
-            raise DomainError(
-                f"capacities sized for {caps.bytes_per_entry} B entries, config implies {bpe} B")
+        ps, sigma, nrm, bpe = _validate(part, profiles, caps, cfg)
         if model not in ("gcn", "sage"):
             raise DomainError(f"unknown model {model!r}")
         if any(int(f) % 4 for f in cfg.f_dim):
@@ -187,12 +323,7 @@ class TrainSession:
         device = torch.cuda.current_device()
         self.comm = DistComm(device) if world > 1 else SoloComm()
 
-        # importance ranking + warm (simulator.py:186-196), native and bit-exact
-        union, score = HG.influence_scores(g, ps)
-        ranked = [h[np.lexsort((h, -score[np.searchsorted(union, h)]))] for h in ps.halo]
-        self.planner = SequentialPlanner(cfg.policy, caps.c_cpu, caps.c_gpu, union, score,
-                                         [np.asarray(h, np.int64) for h in ps.halo], ranked)
-        self.planner.warm()
+        self.planner = _ranked_planner(g, ps, caps, cfg)
         # compact HBM layout when no row is ever staged nor read from a slab
         compact = (cfg.policy == "jaca" and cfg.staleness_bound < 0 and
                    all(int(c) >= h.size for c, h in zip(caps.c_gpu, ps.halo)))
@@ -255,7 +386,7 @@ class TrainSession:
         self._pending = []
 
     def _record(self, stt) -> None:
-        rep, ps, cfg, e = self.rep, self.ps, self.cfg, stt.epoch
+        rep, e = self.rep, stt.epoch
         rep.losses.append(stt.loss)
         rep.epoch_seconds.append(stt.seconds)
         rep.spmm_fwd_ms.append(stt.spmm_fwd_ms)
@@ -264,20 +395,8 @@ class TrainSession:
         if self.keep_logits == "all":
             rep.logits_per_epoch.append(_gather_logits(self.engine, self.comm,
                                                        self.g.n_vertices))
-        dts = []
-        for i in range(ps.P):
-            lh, gh, ms = (int(x) for x in stt.counts[i])
-            self.tot += (lh, gh, ms)
-            c = (ms + ps.cut_edges[i]) * self.mix[i] * cfg.unit_time
-            ov = min(1.0, cfg.prefetch_depth / max(1, len(ps.halo[i])))
-            resid = c - min(c, self.comp[i]) * ov
-            dt = self.comp[i] + resid
-            dts.append(dt)
-            self.records.append(EpochDeviceRecord(
-                epoch=e, device=i, fwd_bytes=ms * self.bpe, bwd_bytes=ps.cut_edges[i] * self.bpe,
-                local_hits=lh, global_hits=gh, misses=ms, compute_time=self.comp[i],
-                comm_time=c, residual_comm_time=resid, device_time=dt))
-        self.spans.append(max(dts))
+        self.spans.append(_epoch_records(self.ps, self.cfg, self.mix, self.comp, self.bpe, e,
+                                         stt.counts, self.tot, self.records))
         if self.record_trace:
             oc = self.engine.gpu_outcomes() if stt.planner == "gpu" else None
             self.rows += _trace_rows(self.planner, e, oc)

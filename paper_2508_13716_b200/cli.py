@@ -1,5 +1,7 @@
-"""Command line: ``train`` (the drop-in for ``halopart simulate``) and
-``profile`` (K9: B200 DeviceProfile rows for ``halopart partition``).
+"""Command line: ``train`` (the drop-in for ``halopart simulate``),
+``cache-bench`` (halopart's policy x capacity grid, plan-only on the native
+planner or with real GPU epochs) and ``profile`` (K9: B200 DeviceProfile
+rows for ``halopart partition``).
 
     python -m paper_2508_13716_b200.cli train --graph g.txt \\
         --partition-result rapa.json --devices devices.json --out run/
@@ -108,9 +110,13 @@ def _load_profiles(devices_opt, P: int):
             "builtin:reference_devices.json", hashlib.sha256(blob).hexdigest())
 
 
-def cmd_train(args) -> int:
-    from . import api
-    opts = _options(args, _TRAIN_DEFAULTS)
+_BENCH_DEFAULTS = {**_TRAIN_DEFAULTS, "policies": "jaca,fifo,lru", "capacities": None,
+                   "train": False}
+
+
+def _sim_inputs(opts: dict):
+    """Graph, partition result, device profiles, capacities and SimConfig
+    from the resolved options (halopart simulate's inputs, cli.py:230-285)."""
     _needed(opts, ("graph", "--graph"), ("partition_result", "--partition-result"))
     opts["fdim"] = _int_list(opts["fdim"])
     graph_path = Path(opts["graph"])
@@ -136,6 +142,22 @@ def cmd_train(args) -> int:
                        prefetch_depth=int(opts["prefetch_depth"]), policy=str(opts["policy"]),
                        f_dim=tuple(fdim), L=L, seed=int(opts["seed"]),
                        unit_time=float(opts["unit_time"]))
+    inputs = {"graph": {"path": str(opts["graph"]), "sha256": A.sha256_file(graph_path)},
+              "partition_result": {"path": str(opts["partition_result"]),
+                                   "sha256": A.sha256_file(result_path)},
+              "devices": {"path": dev_path, "sha256": dev_digest}}
+    return g, result, ps, profiles, caps, cfg, inputs
+
+
+def _manifest(command: str, opts: dict, inputs: dict) -> dict:
+    return {"tool": "paper_2508_13716_b200", "tool_version": __version__, "command": command,
+            "config": {k: v for k, v in opts.items() if k != "out"}, "inputs": inputs}
+
+
+def cmd_train(args) -> int:
+    from . import api
+    opts = _options(args, _TRAIN_DEFAULTS)
+    g, result, ps, profiles, caps, cfg, inputs = _sim_inputs(opts)
     rep = api.train(g, result, profiles, caps, cfg, record_trace=bool(opts["trace"]),
                     model=str(opts["model"]), num_classes=int(opts["classes"]),
                     gemm=str(opts["gemm"]), keep_logits="none", seed=int(opts["weight_seed"]))
@@ -148,17 +170,34 @@ def cmd_train(args) -> int:
                  "train_report.json": A.canon_json(train_doc)}
     if rep.trace_csv is not None:
         artifacts["trace.csv"] = rep.trace_csv.encode("utf-8")
-    manifest = {"tool": "paper_2508_13716_b200", "tool_version": __version__,
-                "command": "train",
-                "config": {k: v for k, v in opts.items() if k != "out"},
-                "inputs": {"graph": {"path": str(opts["graph"]),
-                                     "sha256": A.sha256_file(graph_path)},
-                           "partition_result": {"path": str(opts["partition_result"]),
-                                                "sha256": A.sha256_file(result_path)},
-                           "devices": {"path": dev_path, "sha256": dev_digest}}}
+    manifest = _manifest("train", opts, inputs)
     manifest["config"]["resolved_capacities"] = {
         "c_cpu": caps.c_cpu, "c_gpu": list(caps.c_gpu), "bytes_per_entry": caps.bytes_per_entry}
     A.emit(opts["out"], artifacts, manifest)
+    return 0
+
+
+def cmd_cache_bench(args) -> int:
+    """halopart cache-bench (cli.py:288-301): the workload under several
+    policies and capacities -> compare.csv (byte-identical to the
+    reference's), plan-only on the host, or real GPU epochs with --train."""
+    from . import api
+    opts = _options(args, _BENCH_DEFAULTS)
+    _needed(opts, ("capacities", "--capacities"))
+    caps_list = _int_list(opts["capacities"])
+    pol = opts["policies"]
+    policies = [x for x in pol.replace(",", " ").split()] if isinstance(pol, str) else list(pol)
+    if not caps_list:
+        raise DomainError("need at least one capacity")
+    opts["policy"] = policies[0]
+    g, result, ps, profiles, _, cfg, inputs = _sim_inputs(opts)
+    kw = dict(train_epochs=True, model=str(opts["model"]), num_classes=int(opts["classes"]),
+              gemm=str(opts["gemm"]), keep_logits="none", seed=int(opts["weight_seed"])) \
+        if opts["train"] else {}
+    table = api.compare_policies(g, result, profiles, cfg, policies=policies,
+                                 capacities=caps_list, **kw)
+    A.emit(opts["out"], {"compare.csv": table.to_csv().encode("utf-8")},
+           _manifest("cache-bench", opts, inputs))
     return 0
 
 
@@ -191,6 +230,19 @@ def build_parser() -> argparse.ArgumentParser:
     t.add_argument("--compact-ids", action="store_true", default=None)
     t.add_argument("--trace", action="store_true", default=None)
     t.set_defaults(func=cmd_train)
+    b = sub.add_parser("cache-bench", help="halopart cache-bench: policies x capacities "
+                                           "(plan-only; --train runs GPU epochs)")
+    b.add_argument("--config")
+    for flag, typ in (("graph", str), ("devices", str), ("out", str), ("seed", int),
+                      ("alpha", float), ("fdim", str), ("partition-result", str),
+                      ("epochs", int), ("staleness", int), ("prefetch-depth", int),
+                      ("layers", int), ("unit-time", float), ("policies", str),
+                      ("capacities", str), ("model", str), ("classes", int), ("gemm", str),
+                      ("weight-seed", int)):
+        b.add_argument(f"--{flag}", type=typ, default=None)
+    b.add_argument("--compact-ids", action="store_true", default=None)
+    b.add_argument("--train", action="store_true", default=None)
+    b.set_defaults(func=cmd_cache_bench)
     p = sub.add_parser("profile", help="K9: measure DeviceProfile rows of the visible B200s")
     p.add_argument("--config")
     for flag, typ in (("out", str), ("n", int), ("reps", int), ("density", float),

@@ -158,6 +158,8 @@ k_spmm(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
     constexpr int UNR = (NCH == 1) ? SPMM_UNR1 : SPMM_UNR2;   // rows in flight per lane
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    uint64_t pol_first;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
     const int lane = threadIdx.x & (G - 1);
     const unsigned gmask = (G == 32) ? 0xffffffffu
                                      : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
@@ -253,7 +255,12 @@ k_spmm(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
                 o.z = m.z > 0.f ? o.z : 0.f;
                 o.w = m.w > 0.f ? o.w : 0.f;
             }
-            reinterpret_cast<float4 *>(out + r * ldo)[ch] = o;
+            // written once, never re-read by this launch: evict_first (see
+            // spmm_async.cu), so the output does not displace gathered rows
+            asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;"
+                         ::"l"(reinterpret_cast<float4 *>(out + r * ldo) + ch), "f"(o.x), "f"(o.y),
+                         "f"(o.z), "f"(o.w), "l"(pol_first)
+                         : "memory");
         }
         // rotate the pipeline
         b0 = b1; e0 = e1; s0 = s1;

@@ -26,10 +26,14 @@ extern int cg_cuda_fail(cudaError_t e, const char *what);
 
 namespace cpa {
 
-// CG_SPMM_FLAGS (experiments): bit 0 evict_first output stores, bit 1
-// streaming output stores, bit 2 evict_normal (not evict_last) gathers
+// L2 policies, CG_SPMM_FLAGS: bit 0 evict_first output stores, bit 1
+// streaming output stores, bit 2 evict_normal (not evict_last) gathers.
+// Default 1: the output rows are written once and never re-read by the
+// launch, so they should not displace gathered source rows (C2 sweep,
+// profiles/r02/spmm_sweep.txt: 0.770 -> 0.753 ms of SpMM per epoch; .cs
+// stores and evict_normal gathers gain nothing)
 static int spmm_flags() {
-    static const int f = getenv("CG_SPMM_FLAGS") ? atoi(getenv("CG_SPMM_FLAGS")) : 0;
+    static const int f = getenv("CG_SPMM_FLAGS") ? atoi(getenv("CG_SPMM_FLAGS")) : 1;
     return f;
 }
 

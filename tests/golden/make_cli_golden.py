@@ -30,6 +30,9 @@ import halopart as hp  # noqa: E402
 SIM_FLAGS = ["--epochs", "5", "--staleness", "1", "--capacity", "40", "--fdim", "16,32",
              "--layers", "2", "--policy", "jaca"]
 
+BENCH_FLAGS = ["--epochs", "4", "--staleness", "1", "--fdim", "16,32", "--layers", "2",
+               "--policies", "jaca,fifo,lru", "--capacities", "0,20,40,200"]
+
 
 def main():
     os.makedirs(HERE, exist_ok=True)
@@ -67,6 +70,11 @@ def main():
         assert r.returncode == 0, r.stderr
         js = open(os.path.join(tmp, "sim", "sim_report.json"), "rb").read()
         cs = open(os.path.join(tmp, "sim", "sim_report.csv"), "rb").read()
+        r = run("cache-bench", "--graph", os.path.join(HERE, "graph.txt"), "--partition-result",
+                os.path.join(HERE, "rapa.json"), "--devices", os.path.join(HERE, "devices.json"),
+                *BENCH_FLAGS, "--out", os.path.join(tmp, "bench"))
+        assert r.returncode == 0, r.stderr
+        cmp_csv = open(os.path.join(tmp, "bench", "compare.csv"), "rb").read()
     doc = json.loads(rapa)
     pruned = sum(1 for p in doc["partitions"] if len(p["halo"]) == 0)
     exp = {"sim_flags": SIM_FLAGS, "reference": "halopart " + hp.__version__,
@@ -75,7 +83,8 @@ def main():
            "sim_report_csv_sha256": hashlib.sha256(cs).hexdigest(),
            "sigma": doc["sigma"], "feasible": doc["feasible"],
            "halo_sizes": [len(p["halo"]) for p in doc["partitions"]],
-           "rapa_json_sha256": hashlib.sha256(rapa).hexdigest()}
+           "rapa_json_sha256": hashlib.sha256(rapa).hexdigest(),
+           "bench_flags": BENCH_FLAGS, "compare_csv": cmp_csv.decode("utf-8")}
     with open(os.path.join(HERE, "expected.json"), "w") as fh:
         json.dump(exp, fh, indent=1)
     print(json.dumps(exp, indent=1), "empty halos:", pruned)

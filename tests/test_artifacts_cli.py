@@ -141,3 +141,19 @@ def test_cli_profile_rows_load(tmp_path):
     assert cli.main(["profile", "--n", "2048", "--reps", "3", "--out", str(out)]) == 0
     rows = A.load_device_profiles(out)
     assert rows and all(p.mm_s > 0 and p.mem_gb > 1 for p in rows)
+
+
+def test_cli_cache_bench_reproduces_reference_compare_csv(tmp_path):
+    """`cache-bench` (plan-only, native planner, no GPU) writes the same
+    compare.csv as `halopart cache-bench` on the same inputs."""
+    exp = _exp()
+    out = tmp_path / "bench"
+    rc = cli.main(["cache-bench", "--graph", os.path.join(GOLD, "graph.txt"),
+                   "--partition-result", os.path.join(GOLD, "rapa.json"),
+                   "--devices", os.path.join(GOLD, "devices.json"), *exp["bench_flags"],
+                   "--out", str(out)])
+    assert rc == 0
+    assert (out / "compare.csv").read_text() == exp["compare_csv"]
+    man = json.loads((out / "manifest.json").read_text())
+    assert man["command"] == "cache-bench" and man["outputs"][-1] == "manifest.json"
+    assert cli.main(["cache-bench", "--graph", os.path.join(GOLD, "graph.txt")]) == 2

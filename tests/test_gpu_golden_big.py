@@ -10,7 +10,7 @@
   capacities at s = -1, and a capacity-limited run with misses, global hits
   and write-through: C4 u1000000_s1, C3 u100000_s0).  Fixtures:
   tests/golden/make_golden_big.py ran halopart itself.
-* Float parity at full size: the logits of 256 sampled vertices, for
+* Float parity at full size: the logits of 256 (C4) / 64 (C3) sampled vertices, for
   weight-forced epochs 1-2 of the auto run, vs the float64 sampled-row oracle
   (oracle/sampled_port.py, the model_port semantics over each sample's
   receptive field) within 1e-5 relative (3xTF32 tcgen05 GEMMs).
@@ -46,7 +46,6 @@ _CACHE = {}
 def _workload(name):
     if name in _CACHE:
         return _CACHE[name]
-    _CACHE.clear()   # one large shape resident at a time
     from paper_2508_13716_b200 import hostgraph as H
     s = SHAPES[name]
     gold = load_json(f"{name}.json")
@@ -131,7 +130,9 @@ def test_auto_report_and_sampled_float_parity(name):
     _report_checks(rep, run)
     sg = osp.SampledGraph(g.in_offsets, g.in_targets, parts, s["kind"])
     rng = np.random.default_rng(7)
-    samples = rng.choice(s["n"], 256, replace=False)
+    # C3's average in-degree is 492: 64 samples already reach ~13% of the
+    # graph at layer 1 (and every vertex at layer 0)
+    samples = rng.choice(s["n"], 256 if name == "c4" else 64, replace=False)
     dims = list(s["f_dim"]) + [s["C"]]
     smp, want = osp.sampled_logits(sg, dims, rep.params_per_epoch, samples)
     for e, w in enumerate(want):
