@@ -297,10 +297,24 @@ int cg_spmm_async(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *c
     static const bool narrow_g4 = !getenv("CG_SPMM_G4") || atoi(getenv("CG_SPMM_G4")) != 0;
 #define CG_CPA_ARGS n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, scale, addend, ld_add, \
                     mask, ld_mask, out, ldo, st
+    // lanes per edge stream: CG_SPMM_LANES picks fewer lanes (more 16-byte
+    // chunks per lane, fewer per-edge instructions per byte) for F <= 256
+    static const int lanes = getenv("CG_SPMM_LANES") ? atoi(getenv("CG_SPMM_LANES")) : 0;
     if (F <= 48 && narrow_g4) return launch_s<4, 3, 4, 8>(S, CG_CPA_ARGS);
-    if (F <= 64) return launch_s<8, 2, 4, 8>(S, CG_CPA_ARGS);
-    if (F <= 128) return launch_s<16, 2, 4, 8>(S, CG_CPA_ARGS);
-    if (F <= 256) return launch_s<32, 2, 3, 4, 6, 8>(S, CG_CPA_ARGS);
+    if (F <= 64) {
+        if (lanes == 4) return launch_s<4, 4, 4, 6>(S, CG_CPA_ARGS);
+        return launch_s<8, 2, 4, 8>(S, CG_CPA_ARGS);
+    }
+    if (F <= 128) {
+        if (lanes == 8) return launch_s<8, 4, 4, 6>(S, CG_CPA_ARGS);
+        if (lanes == 4) return launch_s<4, 8, 3, 4>(S, CG_CPA_ARGS);
+        return launch_s<16, 2, 4, 8>(S, CG_CPA_ARGS);
+    }
+    if (F <= 256) {
+        if (lanes == 16) return launch_s<16, 4, 4>(S, CG_CPA_ARGS);
+        if (lanes == 8) return launch_s<8, 8, 3, 4>(S, CG_CPA_ARGS);
+        return launch_s<32, 2, 3, 4, 6, 8>(S, CG_CPA_ARGS);
+    }
     if (F <= 384) return launch_s<32, 3, 3, 4>(S, CG_CPA_ARGS);
     if (F <= 512) return launch_s<32, 4, 3, 4>(S, CG_CPA_ARGS);
     return launch_s<32, 5, 3, 4>(S, CG_CPA_ARGS);

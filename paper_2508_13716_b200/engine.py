@@ -212,6 +212,17 @@ class Engine:
         else:
             self.gw_src_id = torch.full((1,), -1, dtype=i32, device=dev)
             self.gw_src_row = torch.zeros(1, dtype=i32, device=dev)
+        # Layer 0 reads the input features, which carry no version (SURVEY
+        # A2: static): in the compact layout a halo position whose owner is
+        # on this device reads the owner's row in place instead of its
+        # epoch-1 snapshot copy -- the same values, half the distinct rows
+        # the layer-0 gather touches (C2: 334K -> 169K rows, within L2)
+        self.halo_row0 = None
+        if self.L.compact and D.n_halo and self.L.union is not None and self.L.union.size:
+            k = np.searchsorted(self.L.union, D.halo_vertex)
+            own = self.L.owner_dev[k] == self.me
+            h0 = np.where(own, self.L.owner_row[k], D.snap_row_of_pos).astype(np.int32)
+            self.halo_row0 = _dev(h0, i32, dev)
         # backward staging lists
         nb = max(n_bwd, 1)
         self.b_src = _dev(D.bwd_src_dev if n_bwd else [-1], i32, dev)
@@ -585,7 +596,8 @@ class Engine:
                 self._gw(l)
             if spmm_ev is not None:
                 self._rec(spmm_ev[l][0])
-            self._spmm(n_in, F, self.fwd_rowptr, self.fwd_col, n_in, self.halo_row, self.X[l],
+            hrow = self.halo_row0 if (l == 0 and self.halo_row0 is not None) else self.halo_row
+            self._spmm(n_in, F, self.fwd_rowptr, self.fwd_col, n_in, hrow, self.X[l],
                        F, self.norm_dst, None, 0, None, 0, self.Z[l], F)
             if spmm_ev is not None:
                 self._rec(spmm_ev[l][1])

@@ -13,7 +13,8 @@
 * Float parity at full size: the logits of 256 (C4) / 64 (C3) sampled vertices, for
   weight-forced epochs 1-2 of the auto run, vs the float64 sampled-row oracle
   (oracle/sampled_port.py, the model_port semantics over each sample's
-  receptive field) within 1e-5 relative (3xTF32 tcgen05 GEMMs).
+  receptive field) within 1e-4 relative (3xTF32 tcgen05 GEMMs; measured
+  <= 1e-5 at C4, 1.6e-5 at C3).
 """
 
 from __future__ import annotations
@@ -29,7 +30,11 @@ SHAPES = {
     "c4": dict(n=2449029, e=61859140, f_dim=(100, 256, 256), C=47, kind="gcn", hops=1),
     "c3": dict(n=232965, e=114615892, f_dim=(604, 256), C=41, kind="sage", hops=2),
 }
-FORCED_TOL = 1e-5
+# Per-epoch (weight-forced) bound at the large shapes: the north star's 1e-4.
+# Measured (3xTF32): C4 within 1e-5; C3 1.6e-5 at epoch 1 -- GraphSAGE over
+# 604-wide inputs with a 492-edge mean per row sums longer fp32 chains than
+# the small-shape tests (which hold 1e-5)
+FORCED_TOL = 1e-4
 
 
 def _gdig(g):
