@@ -228,12 +228,15 @@ def run_ours(args):
     tot_ms = float(fwd_ms.sum() + bwd_ms.sum())
     achieved = tot_bytes / (tot_ms / 1e3) / 1e9
     peak, peak_kind = peaks()
+    bound = "hbm"
+    if CONFIG == "c3":
+        # C3's gathers are L2 hits (average in-degree 492: the 563 MB feature
+        # matrix is re-read ~200x per epoch), so its roofline is the L2's
+        bound, peak, peak_kind = "l2", l2_peak(), "measured (L2-resident copy, bench.l2_peak)"
     prof = {}
     try:
         with open(os.path.join(ROOT, "profiles", "spmm_traffic.json")) as fh:
-            prof = json.load(fh)
-        if prof.get("config", "c2") != CONFIG:
-            prof = {}   # the committed ncu capture is of another workload
+            prof = json.load(fh).get(CONFIG, {})   # per workload; {} = not captured
     except Exception:  # noqa: BLE001
         pass
 
@@ -317,7 +320,7 @@ def run_ours(args):
                              % (D.n_rows * sum(F_DIM) * 4 / 1e9),
                        "planner": sorted(set(s.planner for s in stats)),
                        "setup_s": round(t_setup, 2)},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,
                          "traffic": prof.get("dram_bytes_per_epoch"),
                          "traffic_basis": "per epoch (sum over the k_spmm launches of one "
@@ -362,6 +365,26 @@ def sum_over_ranks(x, world: int, backend: str):
     t = torch.tensor(np.asarray(x, np.float64), device="cuda" if backend == "nccl" else "cpu")
     dist.all_reduce(t)
     return t.cpu().numpy()
+
+
+def l2_peak(nbytes: int = 24 << 20, reps: int = 50) -> float:
+    """L2 bandwidth, GB/s: a device copy between two L2-resident buffers
+    (2 x 24 MB << 126 MB), read + write bytes, best of 5 batches."""
+    import torch
+    a = torch.empty(nbytes // 4, dtype=torch.float32, device="cuda").uniform_()
+    b = torch.empty_like(a)
+    for _ in range(3):
+        b.copy_(a)
+    best = 1e9
+    for _ in range(5):
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(reps):
+            b.copy_(a)
+        t1.record()
+        torch.cuda.synchronize()
+        best = min(best, t0.elapsed_time(t1) / reps)
+    return 2 * nbytes / (best / 1e3) / 1e9
 
 
 def pcie_peaks(nbytes: int = 256 << 20):

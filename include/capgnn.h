@@ -53,6 +53,16 @@ int cg_ipc_get_handle(void *dev_ptr, uint8_t handle_out[64], int64_t *offset);
 int cg_ipc_open_handle(const uint8_t handle[64], int device, void **dev_ptr);
 int cg_ipc_close_handle(void *dev_ptr);
 
+/* Stream-ordered peer synchronisation (replaces the per-layer collective
+ * barrier between ranks; the reference's "optimistic locks" between the
+ * local / global / prefetch queues).  cg_flag_signal writes
+ * `value` into this rank's flag word on `stream` after its preceding work
+ * (system-scope fence); cg_flag_wait makes `stream` wait until every flag
+ * word flags[i] (device pointers, IPC-mapped for peers; i != skip) is
+ * >= value.  Stream memory operations: no kernel, no host sync.          */
+int cg_flag_signal(uint32_t *flag, uint32_t value, void *stream);
+int cg_flag_wait(const uint64_t *flags, int n, int skip, uint32_t value, void *stream);
+
 /* ---- synthetic inputs (bit-identical to oracle/model_port.py) ---------- */
 /* out[r*ld + k] = uniform_pm1(seed, vertex[r], k) * (row_scale? row_scale[r] : 1) */
 int cg_hash_features(float *out, int64_t ld, const int32_t *vertex, int64_t n_rows,

@@ -51,6 +51,8 @@ SIGNATURES = {
     "cg_scale_rows_to": [P, I64, P, I64, I64, INT, P, P],
     "cg_copy_rows": [I64, INT, P, P, P, P, P, P, I64, P],
     "cg_copy_rows_bounded": [I64, INT, P, P, P, P, P, P, I64, INT, P],
+    "cg_flag_signal": [P, C.c_uint32, P],
+    "cg_flag_wait": [P, INT, INT, C.c_uint32, P],
     "cg_spmm": [I64, INT, P, P, I64, P, P, I64, P, P, I64, P, I64, P, I64, I64, P],
     "cg_gemm": [I64, INT, INT, P, I64, P, INT, P, I64, P, INT, P, INT, P, P, I64, P, I64, INT,
                 P, P, P],

@@ -8,9 +8,15 @@ initialised torch.distributed process group:
   allocation offset) and opened in every process, so the K3 staging kernel
   pulls halo rows straight out of the owner's HBM over NVLink (one-sided,
   no NCCL on the data path);
-* ``barrier()`` is a stream-ordered 1-element NCCL all-reduce: kernels queued
-  after it on this rank's stream cannot start before every rank's preceding
-  kernels (the owners' layer outputs) have completed -- no host sync;
+* ``barrier()`` is stream-ordered: kernels queued after it on this rank's
+  stream cannot start before every rank's preceding kernels (the owners'
+  layer outputs) have completed -- no host sync.  By default it is a
+  point-to-point flag exchange (``cg_flag_signal`` / ``cg_flag_wait``: each
+  rank bumps its own IPC-mapped flag word with a stream write and its stream
+  waits for every peer's word to reach the same generation; stream memory
+  operations, no kernel, no collective).  CG_PEER_SYNC=nccl selects a
+  1-element NCCL all-reduce instead; without CUDA (gloo on CPU) it is a host
+  barrier;
 * ``allreduce_`` is the K7 weight-gradient (+ loss) all-reduce.
 
 The global cache tier is one POSIX shared-memory segment per node, mapped
@@ -64,9 +70,24 @@ class DistComm:
         self._flag = torch.zeros(1, dtype=torch.float32, device=dev)
         self._cuda = torch.cuda.is_available()
         self._opened: list[int] = []
+        mode = os.environ.get("CG_PEER_SYNC", "flags")
+        self.sync = ("flags" if self._cuda and mode == "flags" else
+                     "nccl" if self.backend == "nccl" else "host")
+        if self.sync == "flags":
+            # one 32-bit generation counter per rank, read by every peer
+            self._gen = 0
+            self._word = torch.zeros(16, dtype=torch.int32, device=torch.device("cuda", device))
+            ptrs = self.exchange_pointers(self._word.data_ptr(), device)
+            self._words = np.array(ptrs, np.uint64)
 
     def barrier(self) -> None:
-        if self.backend == "nccl":
+        if self.sync == "flags":
+            import torch
+            self._gen += 1
+            st = torch.cuda.current_stream(self.device).cuda_stream
+            call("cg_flag_signal", self._word.data_ptr(), self._gen, st)
+            call("cg_flag_wait", self._words.ctypes.data, self.world, self.rank, self._gen, st)
+        elif self.sync == "nccl":
             self.dist.all_reduce(self._flag)   # stream-ordered device barrier
         else:
             import torch

@@ -119,4 +119,55 @@ int cg_ipc_close_handle(void *dev_ptr) {
     return e == cudaSuccess ? 0 : cg_cuda_fail(e, "cudaIpcCloseMemHandle");
 }
 
+// ---- stream-ordered peer synchronisation over IPC-mapped flag words -----
+// The per-layer ordering between ranks ("every owner's layer output is
+// final before anyone pulls it") as point-to-point flags instead of a
+// collective: each rank bumps its own flag word on its stream after its
+// preceding kernels (the driver's stream write carries a system-scope
+// fence), and waits on every peer's flag word (IPC-mapped) reaching the same
+// generation before its next kernels.  Stream memory operations run in the
+// stream front-end: no SM, no NCCL kernel, no host synchronisation.
+
+typedef CUresult (*write32_fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*wait32_fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+static int memop_fns(write32_fn *w, wait32_fn *t) {
+    static write32_fn wf = nullptr;
+    static wait32_fn tf = nullptr;
+    if (!wf || !tf) {
+        void *a = nullptr, *b = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        cudaError_t e = cudaGetDriverEntryPoint("cuStreamWriteValue32", &a, cudaEnableDefault, &q);
+        if (e != cudaSuccess || !a) return cg_cuda_fail(e, "cudaGetDriverEntryPoint(cuStreamWriteValue32)");
+        e = cudaGetDriverEntryPoint("cuStreamWaitValue32", &b, cudaEnableDefault, &q);
+        if (e != cudaSuccess || !b) return cg_cuda_fail(e, "cudaGetDriverEntryPoint(cuStreamWaitValue32)");
+        wf = (write32_fn)a;
+        tf = (wait32_fn)b;
+    }
+    *w = wf;
+    *t = tf;
+    return 0;
+}
+
+int cg_flag_signal(uint32_t *flag, uint32_t value, void *stream) {
+    write32_fn w;
+    wait32_fn t;
+    if (memop_fns(&w, &t)) return -1;
+    CUresult r = w((CUstream)stream, (CUdeviceptr)flag, value, CU_STREAM_WRITE_VALUE_DEFAULT);
+    if (r != CUDA_SUCCESS) { cg_set_error("cuStreamWriteValue32 failed"); return -1; }
+    return 0;
+}
+
+int cg_flag_wait(const uint64_t *flags, int n, int skip, uint32_t value, void *stream) {
+    write32_fn w;
+    wait32_fn t;
+    if (memop_fns(&w, &t)) return -1;
+    for (int i = 0; i < n; ++i) {
+        if (i == skip) continue;
+        CUresult r = t((CUstream)stream, (CUdeviceptr)flags[i], value, CU_STREAM_WAIT_VALUE_GEQ);
+        if (r != CUDA_SUCCESS) { cg_set_error("cuStreamWaitValue32 failed"); return -1; }
+    }
+    return 0;
+}
+
 }  // extern "C"

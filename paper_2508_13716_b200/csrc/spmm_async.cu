@@ -306,9 +306,16 @@ int cg_spmm_async(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *c
         return launch_s<8, 2, 4, 8>(S, CG_CPA_ARGS);
     }
     if (F <= 128) {
-        if (lanes == 8) return launch_s<8, 4, 4, 6>(S, CG_CPA_ARGS);
+        // 8-lane streams with 4 chunks per lane (half the per-edge
+        // instructions per byte, twice the rows in flight per warp) win for
+        // the plain forward aggregations (C2 sweep, profiles/r02: 128-wide
+        // 0.088 -> 0.078 ms, 256-wide as two slices 0.197 -> 0.184 ms); the
+        // epilogue variant (addend / mask prefetch registers scale with the
+        // chunks per lane: 150 registers) stays on 16 lanes (0.21 vs 0.33 ms)
+        const bool epi = addend != nullptr || mask != nullptr;
+        if (lanes == 16 || (lanes == 0 && epi)) return launch_s<16, 2, 4, 8>(S, CG_CPA_ARGS);
         if (lanes == 4) return launch_s<4, 8, 3, 4>(S, CG_CPA_ARGS);
-        return launch_s<16, 2, 4, 8>(S, CG_CPA_ARGS);
+        return launch_s<8, 4, 4, 6>(S, CG_CPA_ARGS);
     }
     if (F <= 256) {
         if (lanes == 16) return launch_s<16, 4, 4>(S, CG_CPA_ARGS);
