@@ -302,9 +302,18 @@ def run_ours(args):
                    "exceeds the bench's few-minute budget (see the C2 line)"}
     sess.close()
     del sess, eng
-    exchange = None
+    exchange = exchange_pinned = None
     if CONFIG == "c2" and not args.no_exchange:
         exchange = exchange_record(args, g, ps, world)
+        # the capacity-limited path (C5's shape of cache, at C2 size): small
+        # HBM levels, a large pinned host tier, staleness 1 -> every other
+        # epoch serves ~489K lookups as stale global hits from pinned memory
+        pc = H.CacheCapacities(c_cpu=PINNED_CAP[1], c_gpu=tuple([PINNED_CAP[0]] * ps.P),
+                               bytes_per_entry=caps.bytes_per_entry)
+        exchange_pinned = exchange_record(
+            args, g, ps, world, caps=pc, staleness=1,
+            label=f"C2, c_gpu {PINNED_CAP[0]} per partition, c_cpu {PINNED_CAP[1]} (pinned "
+                  "host tier), staleness 1, JACA")
     if rank == 0:
         line = {
             "metric": "full-batch epoch GTEPS (L*|E|/epoch time)",
@@ -351,6 +360,7 @@ def run_ours(args):
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "exchange": exchange,
+            "exchange_pinned": exchange_pinned,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -407,9 +417,11 @@ def pcie_peaks(nbytes: int = 256 << 20):
 
 
 EXCHANGE_CAP, EXCHANGE_S = 40000, 1
+PINNED_CAP = (20000, 150000)   # (c_gpu per partition, c_cpu)
 
 
-def exchange_record(args, g, ps, world: int, epochs: int = 8):
+def exchange_record(args, g, ps, world: int, epochs: int = 8, caps=None, staleness=None,
+                    label=None):
     """The exchange path, timed: C2 with uniform capacity 40,000 per cache
     level and staleness 1 (the reference-golden case ``u40000_s1``), so every
     epoch has misses, stale global hits served from the pinned host tier,
@@ -419,8 +431,12 @@ def exchange_record(args, g, ps, world: int, epochs: int = 8):
     the reference's model bytes (simulator.py:232-236)."""
     import torch
     from paper_2508_13716_b200 import api, hostgraph as H
-    caps = H.uniform_capacities(ps, EXCHANGE_CAP, F_DIM)
-    cfg = H.SimConfig(epochs=args.warmup + epochs, policy="jaca", staleness_bound=EXCHANGE_S,
+    if caps is None:
+        caps = H.uniform_capacities(ps, EXCHANGE_CAP, F_DIM)
+    staleness = EXCHANGE_S if staleness is None else staleness
+    label = label or (f"C2, uniform capacity {EXCHANGE_CAP} per level (c_gpu, c_cpu), staleness "
+                      f"{EXCHANGE_S}, JACA (reference golden u40000_s1)")
+    cfg = H.SimConfig(epochs=args.warmup + epochs, policy="jaca", staleness_bound=staleness,
                       f_dim=F_DIM, L=len(F_DIM))
     sess = api.TrainSession(g, ps, H.unit_profiles(ps.P), caps, cfg, model=MODEL,
                             num_classes=CLASSES, gemm=args.gemm, keep_logits="none")
@@ -428,7 +444,7 @@ def exchange_record(args, g, ps, world: int, epochs: int = 8):
     eng.k3_timing(True)
     for _ in range(args.warmup):
         sess.step()
-    classes = ("stage", "write_through", "write_back", "grad_pull", "snapshot")
+    classes = ("stage", "prefetch", "write_through", "write_back", "grad_pull", "snapshot")
     tiers = ("stage_host", "stage_peer", "stage_hbm", "write_through", "write_back",
              "grad_pull")
     width = eng.k3_widths()
@@ -440,6 +456,33 @@ def exchange_record(args, g, ps, world: int, epochs: int = 8):
         r = eng.k3_rows()
         rows.append([r[t] for t in tiers])
         counts.append(np.asarray(st.counts).sum(0))
+    # the same epochs with every staging copy in line on the compute stream
+    # (no prefetch queue): how much of the prefetched copies' time it hides
+    eng.prefetch = False
+    eng._graphs = None
+    for _ in range(2):
+        sess.step()
+    nopf_s, nopf_stage = [], []
+    for _ in range(epochs):
+        st = sess.step()
+        nopf_s.append(st.seconds)
+        nopf_stage.append(st.k3.get("stage", 0.0) if st.k3 else 0.0)
+    eng.prefetch = True
+    # the same epochs without request coalescing: every co-resident requester
+    # stages its own copy of a row (the wire rows coalescing saves)
+    eng.coalesce = False
+    eng.k6_static.coalesce = 0
+    eng._graphs = None
+    for _ in range(2):
+        sess.step()
+    noco_s, noco_rows = [], []
+    for _ in range(epochs):
+        st = sess.step()
+        noco_s.append(st.seconds)
+        r = eng.k3_rows()
+        noco_rows.append([r[t] for t in tiers])
+    eng.coalesce = True
+    eng.k6_static.coalesce = 1
     # the same epochs with the host-tier write-through in line on the compute
     # stream (no side-stream queue): how much of its PCIe time the queue hides
     eng.wt_async = False
@@ -452,6 +495,11 @@ def exchange_record(args, g, ps, world: int, epochs: int = 8):
         inl_s.append(st.seconds)
         inl_wt.append(st.k3.get("write_through", 0.0) if st.k3 else 0.0)
     sess.close()
+    noco = max_over_ranks(float(np.mean(noco_s)), world, args.dist_backend)
+    noco_rows = sum_over_ranks(np.asarray(noco_rows, np.float64).mean(0), world,
+                               args.dist_backend)
+    nopf = max_over_ranks(float(np.mean(nopf_s)), world, args.dist_backend)
+    nopf_stage = max_over_ranks(float(np.mean(nopf_stage)), world, args.dist_backend)
     inl = max_over_ranks(float(np.mean(inl_s)), world, args.dist_backend)
     inl_wt = max_over_ranks(float(np.mean(inl_wt)), world, args.dist_backend)
     ep = max_over_ranks(float(np.mean(ep_s)), world, args.dist_backend)
@@ -469,9 +517,8 @@ def exchange_record(args, g, ps, world: int, epochs: int = 8):
         return nbytes / (ms / 1e3) / 1e9 if ms > 0 else None
     stage_bytes = wire["stage_host"] + wire["stage_peer"] + wire["stage_hbm"]
     return {
-        "workload": f"C2, uniform capacity {EXCHANGE_CAP} per level (c_gpu, c_cpu), staleness "
-                    f"{EXCHANGE_S}, JACA (reference golden u40000_s1); epochs "
-                    f"{args.warmup + 1}..{args.warmup + epochs} (K6-planned, period-2 plan)",
+        "workload": f"{label}; epochs {args.warmup + 1}..{args.warmup + epochs} "
+                    "(K6-planned, period-2 plan)",
         "ms_per_epoch": ep * 1e3, "gteps": len(F_DIM) * g.n_edges / ep / 1e9,
         "lookups_per_epoch": {"local_hits": float(cnt[0]), "global_hits": float(cnt[1]),
                               "misses": float(cnt[2])},
@@ -489,6 +536,23 @@ def exchange_record(args, g, ps, world: int, epochs: int = 8):
         "rows_per_epoch": {t: float(rows_tot[i]) for i, t in enumerate(tiers)},
         "k3_ms_per_epoch": k3d,
         "k3_share_of_epoch": sum(k3) / (ep * 1e3),
+        "request_coalescing": {
+            "ms_per_epoch_on": ep * 1e3, "ms_per_epoch_off": noco * 1e3,
+            "rows_per_epoch_off": {t: float(noco_rows[i]) for i, t in enumerate(tiers)},
+            "pcie_read_bytes_per_epoch_off": float(noco_rows[tiers.index("stage_host")])
+                                             * width["stage_host"] * 4,
+            "how": "same session, same epochs with every co-resident requester staging its "
+                   "own copy (CG_COALESCE=0) vs one staged row per (vertex, source, device)"},
+        "prefetch_queue": {
+            "ms_per_epoch_prefetch": ep * 1e3, "ms_per_epoch_inline": nopf * 1e3,
+            "stage_ms_inline": nopf_stage,
+            "stage_ms_with_prefetch": {"inline (owner rows, layers >= 1)": k3d["stage"],
+                                       "prefetch stream": k3d["prefetch"]},
+            "hidden_frac": ((nopf - ep) * 1e3 / nopf_stage) if nopf_stage > 0 else None,
+            "how": "same session, same K6-planned epochs: staging rows final before the epoch "
+                   "(pinned-tier reads of every layer, all layer-0 rows) copied on a prefetch "
+                   "stream right after the plan, the compute stream waiting per layer, vs every "
+                   "staging copy in line; hidden = (inline - prefetch) / inline staging time"},
         "write_through_queue": {
             "ms_per_epoch_queued": ep * 1e3, "ms_per_epoch_inline": inl * 1e3,
             "write_through_ms_inline": inl_wt,
@@ -499,7 +563,7 @@ def exchange_record(args, g, ps, world: int, epochs: int = 8):
                    "the end of the update; one graph per epoch; k3_ms_per_epoch.write_through "
                    "is its side-stream time) vs in line on the compute stream; hidden = "
                    "(inline - queued) / inline write-through time"},
-        "k3_GB_s": {"stage": rate(stage_bytes, k3d["stage"]),
+        "k3_GB_s": {"stage (in line, prefetch off)": rate(stage_bytes, nopf_stage),
                     "write_through": rate(wire["write_through"], k3d["write_through"]),
                     "write_back": rate(wire["write_back"], k3d["write_back"]),
                     "grad_pull": rate(wire["grad_pull"], k3d["grad_pull"])},

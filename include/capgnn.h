@@ -95,6 +95,17 @@ int cg_copy_rows_bounded(int64_t n, int F, const int32_t *src_id, const int32_t 
                          const int32_t *dst_row, const float *const *tab,
                          const int64_t *tab_ld, float *dst, int64_t ld_dst, int max_blocks,
                          void *stream);
+/* The same copy restricted to the entries whose src_id lies in
+ * [id_lo, id_hi) (the others are skipped).  One staging table then feeds
+ * two queues (PAPER.md:98's prefetch queue, R10): the rows that are final
+ * before the epoch starts (the pinned host tier, id = n_dev; every source
+ * of the static layer-0 features) are copied ahead on a prefetch stream,
+ * and only the current-epoch owner rows (ids < n_dev) wait for the
+ * layer's barrier.                                                       */
+int cg_copy_rows_sel(int64_t n, int F, const int32_t *src_id, const int32_t *src_row,
+                     const int32_t *dst_row, const float *const *tab, const int64_t *tab_ld,
+                     float *dst, int64_t ld_dst, int id_lo, int id_hi, int max_blocks,
+                     void *stream);
 
 /* ---- K1/K2: fused cache-lookup + gather SpMM --------------------------- */
 /* out[r] = epi( scale[r] * sum_{e in [rowptr[r], rowptr[r+1])} X[map(col[e])] )
@@ -210,6 +221,11 @@ typedef struct cg_plan_static {
                                    requester's vertex on its device, or -1:
                                    every read at version <= 1 is served
                                    from it; NULL = none      */
+    int32_t coalesce;           /* 1: co-resident requesters of a vertex that
+                                   need the same value this epoch (peer
+                                   owner row / global-tier entry) share the
+                                   row the first one stages (one wire row per
+                                   device); 0: every requester stages       */
 } cg_plan_static;
 
 int cg_plan_frozen(const cg_plan_static *st, int epoch, int staleness, int me,

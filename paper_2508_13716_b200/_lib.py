@@ -28,7 +28,7 @@ class PlanStatic(C.Structure):
                 ("req_pos", P), ("req_slot", P), ("req_needed", P), ("owner_dev", P),
                 ("owner_row", P), ("gslot", P), ("lfree", P), ("score", P), ("lmin", P),
                 ("gmin", F64), ("gfree", I32), ("policy", I32), ("n_parts", I32),
-                ("req_snap", P)]
+                ("req_snap", P), ("coalesce", I32)]
 
 
 # name -> argtypes (restype int unless listed in _RESTYPES)
@@ -51,6 +51,7 @@ SIGNATURES = {
     "cg_scale_rows_to": [P, I64, P, I64, I64, INT, P, P],
     "cg_copy_rows": [I64, INT, P, P, P, P, P, P, I64, P],
     "cg_copy_rows_bounded": [I64, INT, P, P, P, P, P, P, I64, INT, P],
+    "cg_copy_rows_sel": [I64, INT, P, P, P, P, P, P, I64, INT, INT, INT, P],
     "cg_flag_signal": [P, C.c_uint32, P],
     "cg_flag_wait": [P, INT, INT, C.c_uint32, P],
     "cg_spmm": [I64, INT, P, P, I64, P, P, I64, P, P, I64, P, I64, P, I64, I64, P],
@@ -120,7 +121,7 @@ def lib():
 # device entry points report how many kernels they launched; the running
 # total is the bench's "gpu_launches" evidence
 KERNEL_ENTRY = {"cg_hash_features", "cg_hash_labels", "cg_scale_rows", "cg_scale_rows_to",
-                "cg_copy_rows", "cg_copy_rows_bounded",
+                "cg_copy_rows", "cg_copy_rows_bounded", "cg_copy_rows_sel",
                 "cg_spmm", "cg_gemm", "cg_wgrad", "cg_colsum", "cg_softmax_ce", "cg_adam",
                 "cg_split_tf32", "cg_split_tf32_t",
                 "cg_plan_frozen", "cg_set_epoch"}

@@ -82,7 +82,7 @@ __global__ void k_copy_rows(int64_t n, int F, const int32_t *__restrict__ src_id
                             const int32_t *__restrict__ dst_row,
                             const float *const *__restrict__ tab,
                             const int64_t *__restrict__ tab_ld, float *__restrict__ dst,
-                            int64_t ld_dst) {
+                            int64_t ld_dst, int id_lo, int id_hi) {
     pdl_entry();
     // Each warp scans 32 table entries at a time (one per lane), compacts the
     // live ones with a ballot, then copies those rows cooperatively: most
@@ -96,6 +96,7 @@ __global__ void k_copy_rows(int64_t n, int F, const int32_t *__restrict__ src_id
         if (i < n) {
             sid = src_id[i];
             drow = dst_row[i];
+            if (sid < id_lo || sid >= id_hi) sid = -1;   // another queue's entry
             if (sid >= 0 && drow >= 0) srow = src_row[i];
         }
         unsigned live = __ballot_sync(0xffffffffu, sid >= 0 && drow >= 0);
@@ -709,6 +710,12 @@ __device__ __forceinline__ void plan_vertex(const cg_plan_static &st, int64_t u,
     const int32_t g = st.gslot[u];
     const int32_t odev = st.owner_dev[u], orow = st.owner_row[u];
     bool gdirty = false;
+    // request coalescing: co-resident requesters of u that need the same
+    // value this epoch (the owner's current row from a peer, or the global
+    // tier's entry -- one version per epoch: glob_ver changes only on a miss,
+    // which makes it current) read the row the first one staged, so each
+    // distinct row crosses NVLink / PCIe once per device and layer
+    int32_t row_cur = -1, row_glob = -1;
     for (int64_t k = st.req_off[u]; k < st.req_off[u + 1]; ++k) {
         const int32_t slot = st.req_slot[k];
         const int32_t part = st.req_part[k];
@@ -769,19 +776,25 @@ __device__ __forceinline__ void plan_vertex(const cg_plan_static &st, int64_t u,
         int src_id, src_row;
         if (cur) { src_id = odev; src_row = orow; }
         else { src_id = n_devices; src_row = g; }  // host tier (table entry n_devices)
+        int32_t &have = cur ? row_cur : row_glob;
         if (slot >= 0) {  // write through into the local slab, read it there
             stage_src[pos] = src_id;
             stage_row[pos] = src_row;
             stage_dst[pos] = slot;
             halo_row[pos] = slot;
+            if (have < 0) have = slot;
         } else if (cur && odev == me) {  // co-resident owner: read in place
             stage_src[pos] = -1;
             halo_row[pos] = orow;
+        } else if (st.coalesce && have >= 0) {  // already staged on this device this epoch
+            stage_src[pos] = -1;
+            halo_row[pos] = have;
         } else {
             stage_src[pos] = src_id;
             stage_row[pos] = src_row;
             stage_dst[pos] = staging_base + pos;
             halo_row[pos] = staging_base + pos;
+            have = staging_base + pos;
         }
     }
     if (odev == me) {
@@ -902,23 +915,33 @@ int cg_hash_labels(int32_t *out, const int32_t *vertex, int64_t n_rows, int C, u
     return 1;
 }
 
-int cg_copy_rows_bounded(int64_t n, int F, const int32_t *src_id, const int32_t *src_row,
-                         const int32_t *dst_row, const float *const *tab,
-                         const int64_t *tab_ld, float *dst, int64_t ld_dst, int max_blocks,
-                         void *stream) {
+int cg_copy_rows_sel(int64_t n, int F, const int32_t *src_id, const int32_t *src_row,
+                     const int32_t *dst_row, const float *const *tab, const int64_t *tab_ld,
+                     float *dst, int64_t ld_dst, int id_lo, int id_hi, int max_blocks,
+                     void *stream) {
     if (n == 0) return 0;
+    if (id_lo < 0) id_lo = 0;
+    if (id_hi <= id_lo) return 0;
     const int threads = 256;
     int blocks = grid_for(n, threads, max_blocks > 0 ? max_blocks : 148 * 32);
     bool vec = (F % 4 == 0) && (ld_dst % 4 == 0) && ((uintptr_t)dst % 16 == 0);
     // source alignment is validated on the host side (tab_ld % 4 == 0, 16-B bases)
     if (vec)
         cgpdl::launch(k_copy_rows<true>, dim3(blocks), dim3(threads), 0, (cudaStream_t)stream, n,
-                      F, src_id, src_row, dst_row, tab, tab_ld, dst, ld_dst);
+                      F, src_id, src_row, dst_row, tab, tab_ld, dst, ld_dst, id_lo, id_hi);
     else
         cgpdl::launch(k_copy_rows<false>, dim3(blocks), dim3(threads), 0, (cudaStream_t)stream, n,
-                      F, src_id, src_row, dst_row, tab, tab_ld, dst, ld_dst);
+                      F, src_id, src_row, dst_row, tab, tab_ld, dst, ld_dst, id_lo, id_hi);
     CG_CHECK_LAUNCH("k_copy_rows");
     return 1;
+}
+
+int cg_copy_rows_bounded(int64_t n, int F, const int32_t *src_id, const int32_t *src_row,
+                         const int32_t *dst_row, const float *const *tab,
+                         const int64_t *tab_ld, float *dst, int64_t ld_dst, int max_blocks,
+                         void *stream) {
+    return cg_copy_rows_sel(n, F, src_id, src_row, dst_row, tab, tab_ld, dst, ld_dst, 0,
+                            0x7fffffff, max_blocks, stream);
 }
 
 int cg_copy_rows(int64_t n, int F, const int32_t *src_id, const int32_t *src_row,

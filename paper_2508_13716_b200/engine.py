@@ -87,6 +87,13 @@ class Engine:
         self.wt_async = os.environ.get("CG_WT_ASYNC", "1") != "0"
         self._wt_early = True
         self._wt = None
+        # R10 prefetch queue: staging rows that are final
+        # before the epoch starts are copied ahead on a side stream
+        self.prefetch = os.environ.get("CG_PREFETCH", "1") != "0"
+        # request coalescing of staged rows (K6 / host tables); CG_COALESCE=0
+        # stages every requester's row (the A/B reference)
+        self.coalesce = os.environ.get("CG_COALESCE", "1") != "0"
+        self._pf = None
         self._alloc(caps, params_init)
         if self._gw_active():
             # the write-through queue: side stream + fork/join events, made
@@ -96,6 +103,12 @@ class Engine:
                             fork=[torch.cuda.Event() for _ in range(self.nL)],
                             done=[torch.cuda.Event() for _ in range(self.nL)])
             for ev in self._wt["fork"] + self._wt["done"]:
+                ev.record(cs)
+        if self.D.n_halo and not self.L.compact:
+            cs = torch.cuda.current_stream(self.dev)
+            self._pf = dict(stream=torch.cuda.Stream(self.dev), fork=torch.cuda.Event(),
+                            done=[torch.cuda.Event() for _ in range(self.nL)])
+            for ev in [self._pf["fork"]] + self._pf["done"]:
                 ev.record(cs)
 
     def k3_timing(self, on: bool = True, pool: int = 64) -> None:
@@ -345,6 +358,12 @@ class Engine:
         wb_src, wb_dst = [], []
         if L.union is not None and L.union.size:
             hoff = L.halo_off
+            # request coalescing (as K6): per union vertex, the first staging
+            # row this epoch that receives the owner's current row from a
+            # peer / the global tier's entry (one version per epoch); later
+            # co-resident requesters read that row instead of staging again
+            first_cur = np.full(L.union.size, -1, np.int64)
+            first_glob = np.full(L.union.size, -1, np.int64)
             for p in D.parts:
                 b, eidx = hoff[p], hoff[p + 1]
                 if eidx == b:
@@ -383,6 +402,15 @@ class Engine:
                     raise RuntimeError("stale global hit without a global slot")
                 s_src[pos[from_host]] = nd
                 s_row[pos[from_host]] = gsl
+                for kind_m, first in (((from_owner, first_cur), (from_host, first_glob))
+                                      if self.coalesce else ()):
+                    j = np.flatnonzero(kind_m)
+                    have = first[k[j]]
+                    dup = have >= 0
+                    halo_row[pos[j[dup]]] = have[dup]
+                    s_dst[pos[j[dup]]] = -1
+                    s_src[pos[j[dup]]] = -1
+                    first[k[j[~dup]]] = n_in + pos[j[~dup]]
                 # write-back of the final local-slot contents (after the SpMM);
                 # slots at version <= 1 are never read (the snapshot serves them)
                 lo, c = int(self.planner.lslot_off[p]), int(self.planner.c_gpu[p])
@@ -460,7 +488,7 @@ class Engine:
             owner_row=ptr(k["owner_row"]), gslot=ptr(k["gslot"]), lfree=ptr(k["lfree"]),
             score=ptr(k["score"]), lmin=ptr(k["lmin"]), gmin=float(stt["gmin"]),
             gfree=int(stt["gfree"]), policy=0 if self.policy == "jaca" else 1, n_parts=L.P,
-            req_snap=ptr(k["req_snap"]))
+            req_snap=ptr(k["req_snap"]), coalesce=int(self.coalesce))
         self.gpu_plan_ready = True
 
     def plan(self, e: int) -> tuple[str, np.ndarray | None, EpochPlan | None]:
@@ -503,15 +531,21 @@ class Engine:
     _k3_on = False
 
     def _copy(self, n, F, src_id, src_row, dst_row, tab, tab_ld, dst, ld, cls="stage",
-              stream=None, max_blocks: int = 0):
+              stream=None, max_blocks: int = 0, ids=None):
         st = stream.cuda_stream if stream is not None else self.stream()
         ev = None
         if self._k3_on and self._k3_used is not None and len(self._k3_used) < len(self._k3_pool):
             ev = self._k3_pool[len(self._k3_used)]
             self._k3_used.append((cls, F, ev))
             self._rec(ev[0], stream)
-        call("cg_copy_rows_bounded", n, F, ptr(src_id), ptr(src_row), ptr(dst_row), ptr(tab),
-             ptr(tab_ld), dst if isinstance(dst, int) else ptr(dst), ld, max_blocks, st)
+        if ids is None:
+            call("cg_copy_rows_bounded", n, F, ptr(src_id), ptr(src_row), ptr(dst_row),
+                 ptr(tab), ptr(tab_ld), dst if isinstance(dst, int) else ptr(dst), ld,
+                 max_blocks, st)
+        else:
+            call("cg_copy_rows_sel", n, F, ptr(src_id), ptr(src_row), ptr(dst_row), ptr(tab),
+                 ptr(tab_ld), dst if isinstance(dst, int) else ptr(dst), ld, ids[0], ids[1],
+                 max_blocks, st)
         if ev is not None:
             self._rec(ev[1], stream)
 
@@ -574,8 +608,41 @@ class Engine:
         else:
             ev.record()
 
+    # R10 prefetch queue (prefetch_depth simulator.py:44,237-239).
+    # Of a layer's staging rows, two kinds are final before the epoch's
+    # forward pass starts: rows read from the pinned host tier (stale global
+    # hits: written through in an EARLIER epoch, and that write-through was
+    # joined before this epoch's plan) and, at layer 0, every row (the input
+    # features are static; re-uploaded inputs land before the fork).  They
+    # are copied on a side stream right after the plan -- the layer-1/2 host
+    # reads (PCIe, ~51 GB/s) then run under layer 0's SpMM / GEMM -- and the
+    # compute stream waits on layer l's copy only before layer l's SpMM.
+    # Only current-epoch owner rows (ids < n_dev) stay in line behind the
+    # layer's barrier.  Safe when no global slot can change hands mid-epoch
+    # under a peer's write-through (_wt_early: one process, or a K6-planned
+    # epoch); otherwise every copy stays in line.  CG_PREFETCH=0 disables it.
+    PF_BLOCKS = int(os.environ.get("CG_PF_BLOCKS", "32"))
+
+    def _prefetch_rows(self) -> bool:
+        pf = self._pf
+        if pf is None or not self.prefetch or not self._wt_early:
+            return False
+        cs = torch.cuda.current_stream(self.dev)
+        pf["fork"].record(cs)
+        pf["stream"].wait_event(pf["fork"])
+        nd = self.L.n_dev
+        for l, F in enumerate(self.F):
+            ids = (0, nd + 1) if l == 0 else (nd, nd + 1)
+            self._copy(self.D.n_halo, F, self.stage_src, self.stage_row, self.stage_dst,
+                       self.tab[l], self.tab_ld[l], self.X[l], F, cls="prefetch",
+                       stream=pf["stream"], max_blocks=0 if l == 0 else self.PF_BLOCKS,
+                       ids=ids)
+            pf["done"][l].record(pf["stream"])
+        return True
+
     def _forward(self, e: int, spmm_ev) -> None:
         D, nL, kind, n_in = self.D, self.nL, self.kind, self.D.n_in
+        pf = self._prefetch_rows()
         for l in range(nL):
             F, Fo = self.F[l], self.dims[l + 1]
             if l > 0:
@@ -587,8 +654,15 @@ class Engine:
                 self._copy(D.n_snap, F, self.snap_src, self.snap_srow, self.snap_dst,
                            self.tab[l], self.tab_ld[l], self.X[l], F, cls="snapshot")
             if D.n_halo and not self.L.compact:   # compact: nothing is ever staged
-                self._copy(D.n_halo, F, self.stage_src, self.stage_row, self.stage_dst,
-                           self.tab[l], self.tab_ld[l], self.X[l], F)
+                if pf:
+                    torch.cuda.current_stream(self.dev).wait_event(self._pf["done"][l])
+                    if l > 0:   # current-epoch owner rows, behind the barrier
+                        self._copy(D.n_halo, F, self.stage_src, self.stage_row,
+                                   self.stage_dst, self.tab[l], self.tab_ld[l], self.X[l], F,
+                                   ids=(0, self.L.n_dev))
+                else:
+                    self._copy(D.n_halo, F, self.stage_src, self.stage_row, self.stage_dst,
+                               self.tab[l], self.tab_ld[l], self.X[l], F)
             if l < nL - 1 and self._wt_early:
                 # this layer's input rows are final and its stale global hits
                 # have been staged (a host-plan epoch may reassign a slot read
@@ -710,9 +784,19 @@ class Engine:
 
     def _update(self) -> None:
         """K7 + optimizer + the weights' TF32 split; uses self.step."""
+        # the write-through queue joins BEFORE K7: a rank's all-reduce then
+        # completes only after every rank's host-tier writes of this epoch,
+        # which the next epoch's prefetch reads
+        self._join_gw()
         self.comm.allreduce_(self.grads)
         if not self._wt_early:
+            # the last layer's write-through goes after every rank's staging
+            # of that layer (the all-reduce orders it), and lands before any
+            # rank's next epoch starts
             self._gw(self.nL - 1)
+            self._join_gw()
+            if self.comm.world > 1:
+                self.comm.barrier()
         call("cg_adam", self.n_params, ptr(self.params), ptr(self.grads), ptr(self.adam_m),
              ptr(self.adam_v), self.lr, 0.9, 0.999, 1e-8, self.step,
              ptr(self.params_hi) if self.params_hi is not None else None,
@@ -720,7 +804,6 @@ class Engine:
              ptr(self.adam_corr) if self._capturing else None, self.stream())
         if self.params_hi is not None:
             self._split_t()
-        self._join_gw()
 
     def _new_timers(self, n: int):
         return [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))

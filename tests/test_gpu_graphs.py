@@ -26,10 +26,8 @@ def _run(case, graphs):
     from paper_2508_13716_b200 import api, hostgraph as H
     kind, n, deg, P, f_dim, C, cap, policy, s, epochs, gemm = case
     g, ps, _, _ = workload(n, deg, P)
-    if cap == "auto":
-        caps = H.compute_capacities(ps, -1, [180.0] * P, 1024.0, 64.0, 2048.0, f_dim, len(f_dim))
-    else:
-        caps = H.uniform_capacities(ps, cap, f_dim)
+    from test_gpu_train_parity import make_caps
+    caps = make_caps(H, ps, cap, f_dim)
     cfg = H.SimConfig(epochs=epochs, policy=policy, staleness_bound=s, f_dim=f_dim, L=len(f_dim))
     rep = api.train(g, ps, H.unit_profiles(P), caps, cfg, model=kind, num_classes=C,
                     keep_logits="all", keep_params=True, record_trace=True, gemm=gemm,
@@ -85,4 +83,31 @@ def test_graph_session_io_pipeline():
     assert ra == rb
     assert np.array_equal(sa, sb)
     for a, b in zip(la, lb):
+        assert np.array_equal(a, b)
+
+
+PF_CASES = [c for c in CASES if c[6] != "auto"] + [
+    ("gcn", 600, 6.0, 4, (16, 32, 32), 7, 40, "jaca", 1, 6, "3xtf32"),
+    ("gcn", 600, 6.0, 4, (16, 32, 32), 7, 40, "fifo", 2, 6, "3xtf32"),
+    ("gcn", 500, 5.0, 4, (16, 32, 32), 6, (20, 200), "jaca", 1, 5, "3xtf32"),
+    ("sage", 600, 6.0, 4, (16, 32, 32), 6, (40, 300), "jaca", 2, 6, "fp32"),
+]
+
+
+@pytest.mark.parametrize("case", PF_CASES, ids=lambda c: f"{c[0]}-{c[7]}-s{c[8]}-cap{c[6]}")
+@pytest.mark.parametrize("graphs", [False, True], ids=["eager", "graphs"])
+def test_prefetch_queue_bit_identical(case, graphs, monkeypatch):
+    """R10: staging rows copied ahead on the prefetch stream (pinned-tier
+    rows of every layer, all layer-0 rows) give exactly the results of the
+    all-in-line staging (same rows, same values; only the stream differs)."""
+    monkeypatch.setenv("CG_PREFETCH", "0")
+    inline = _run(case, graphs)
+    monkeypatch.setenv("CG_PREFETCH", "1")
+    pf = _run(case, graphs)
+    assert [r.__dict__ for r in pf.records] == [r.__dict__ for r in inline.records]
+    assert sum(r.global_hits for r in pf.records) > 0   # the host tier is read
+    assert pf.losses == inline.losses
+    for a, b in zip(pf.logits_per_epoch, inline.logits_per_epoch):
+        assert np.array_equal(a, b)
+    for a, b in zip(pf.params, inline.params):
         assert np.array_equal(a, b)

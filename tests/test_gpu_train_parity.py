@@ -19,6 +19,18 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-4
 
 
+def make_caps(H, ps, cap, f_dim):
+    """"auto" (Algorithm 1), an int (uniform), or (c_gpu, c_cpu)."""
+    if cap == "auto":
+        return H.compute_capacities(ps, -1, [180.0] * ps.P, 1024.0, 64.0, 2048.0, f_dim,
+                                    len(f_dim))
+    if isinstance(cap, tuple):
+        u = H.uniform_capacities(ps, 1, f_dim)
+        return H.CacheCapacities(c_cpu=cap[1], c_gpu=(cap[0],) * ps.P,
+                                 bytes_per_entry=u.bytes_per_entry)
+    return H.uniform_capacities(ps, cap, f_dim)
+
+
 def _train(g, ps, caps, cfg, kind, C, **kw):
     from paper_2508_13716_b200 import api, hostgraph as H
     return api.train(g, ps, H.unit_profiles(ps.P), caps, cfg, model=kind, num_classes=C,
@@ -47,6 +59,11 @@ CASES = [
     # one layer (the logits gradient is never aggregated): narrow and wide C
     ("gcn", 400, 6.0, 4, (32,), 7, 60, "jaca", 1, 3, "3xtf32"),
     ("sage", 400, 6.0, 4, (16,), 40, "auto", "jaca", -1, 3, "3xtf32"),
+    # small HBM levels beside a large pinned tier (c_gpu, c_cpu): stale global
+    # hits read the host tier, several co-resident requesters per vertex
+    # (request coalescing: one staged row per vertex and device)
+    ("gcn", 500, 5.0, 4, (16, 32, 32), 6, (20, 200), "jaca", 1, 5, "3xtf32"),
+    ("sage", 600, 6.0, 4, (16, 32, 32), 6, (40, 300), "jaca", 2, 6, "3xtf32"),
     # the SIMT fp32 GEMM (explicit opt-in)
     ("gcn", 500, 5.0, 3, (16, 32, 32), 6, 60, "jaca", 1, 4, "fp32"),
     ("sage", 400, 6.0, 4, (16, 32, 32), 7, "auto", "jaca", -1, 3, "fp32"),
@@ -59,10 +76,7 @@ def test_train_matches_oracle(case):
     from paper_2508_13716_b200 import hostgraph as H
     kind, n, deg, P, f_dim, C, cap, policy, s, epochs, gemm = case
     g, ps, og, ops = workload(n, deg, P)
-    if cap == "auto":
-        caps = H.compute_capacities(ps, -1, [180.0] * P, 1024.0, 64.0, 2048.0, f_dim, len(f_dim))
-    else:
-        caps = H.uniform_capacities(ps, cap, f_dim)
+    caps = make_caps(H, ps, cap, f_dim)
     cfg = H.SimConfig(epochs=epochs, policy=policy, staleness_bound=s, f_dim=f_dim,
                       L=len(f_dim))
     rep = _train(g, ps, caps, cfg, kind, C, record_trace=True, gemm=gemm)
