@@ -79,6 +79,12 @@ struct Params {
     int tma_store;   // C written by TMA bulk tensor stores (mC is valid)
     int tma_mask;    // ReLU-backward mask tiles TMA-loaded into the store staging (mM)
     int nbuf;        // staging buffers per epilogue warp (2, or 4 to prefetch masks)
+    int bres;        // B resident: the CTA's whole B slice (hi + lo, every k-block) is
+                     // TMA-loaded into smem once and the ring streams A only
+    int ring_off;    // byte offset of the stage ring (= resident B bytes, 1024-aligned)
+    int bres_kb;     // bytes per resident k-block of B (hi; lo at bres_lo_off)
+    int bres_lo_off;
+    int pf_dist;     // k-blocks the L2 prefetch cursor runs ahead of the TMA loads
     float *bws;      // weight gradient only: per (chunk, splitter warp) column sums
                      // of the MN-major B operand (= the bias gradient partials)
     int dbg;         // diagnostics only (CG_GEMM_DBG, wrong results): 1 = splitter
@@ -194,6 +200,15 @@ __device__ __forceinline__ void tma_load_3d(const CUtensorMap *map, uint64_t *ba
         : "memory");
 }
 
+// L2 prefetch of a TMA box (no smem, no barrier): runs the operand stream
+// further ahead of the smem ring than its stage count allows
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap *map, int x, int y) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(x), "r"(y)
+                 : "memory");
+}
+
 // C tile store: smem (128B-swizzled, 32 rows x 32 fp32) -> global via TMA;
 // the tensor map clips rows >= M and columns >= N.
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, const void *src, int x, int y,
@@ -266,6 +281,42 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Split-phase TMEM load: issue a 32-column load, then wait for it later
+// with the registers passed as read-write operands, so no use of them can
+// be scheduled between the issue and the wait (the next chunk's load is in
+// flight while the current chunk is processed).
+__device__ __forceinline__ void tmem_ld32_issue(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+          "=r"(r[31])
+        : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_ld32_wait(uint32_t (&r)[32]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]),
+                   "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]),
+                   "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]), "+r"(r[16]),
+                   "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                   "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]),
+                   "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+                 :
+                 : "memory");
+}
+
+// Compile-time epilogue variants (the TMA-store path): bit 0 bias, bit 1
+// ReLU, bit 2 row scale, bit 3 ReLU-backward mask (TMA-loaded).  EPI_GENERIC
+// keeps every operand a runtime switch (direct stores, unaligned shapes,
+// the diagnostics knobs).
+constexpr int EPI_BIAS = 1, EPI_RELU = 2, EPI_RS = 4, EPI_MASK = 8, EPI_GENERIC = -1;
+
 // Tile t of the persistent schedule -> (m tile, n tile, split-K chunk);
 // consecutive t share the m tile so concurrently running CTAs reuse the A
 // rows through L2.
@@ -305,6 +356,7 @@ __device__ __forceinline__ void kblocks(const Params &p, int o, int z, int &begi
 // Persistent warp-specialised kernel: the smem stage ring and the two TMEM
 // accumulator buffers run continuously across this CTA's tiles, so the
 // epilogue of tile i overlaps the TMA + MMA of tile i+1.
+template <int EPI>
 __global__ void __launch_bounds__(THREADS, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mB0,
           const __grid_constant__ CUtensorMap mA1, const __grid_constant__ CUtensorMap mB1,
@@ -314,7 +366,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
     // no static shared memory in this kernel, so the dynamic window starts
     // 1024-byte aligned (required by the 128B-swizzle atoms); pointers stay
     // derived from the __shared__ array so accesses compile to LDS/STS
-    extern __shared__ __align__(1024) uint8_t smem[];
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = smem_raw + p.ring_off;   // the stage ring (after any resident B)
     const int S = p.stages;
     const int HI_BYTES = p.hi_bytes;
     const int stage_bytes = p.stage_bytes;
@@ -325,7 +378,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
     uint64_t *tfull = empty + S;   // [2] accumulator ready
     uint64_t *tempty = tfull + 2;  // [2] accumulator drained
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
-    uint64_t *mbar_mask = tempty + 3;  // [4 warps][nbuf] mask-tile arrivals
+    uint64_t *bres_bar = tempty + 3;   // resident B landed
+    uint64_t *mbar_mask = tempty + 4;  // [4 warps][nbuf] mask-tile arrivals
 
     // warp index made provably warp-uniform (shfl) so role branches do not diverge
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
@@ -345,6 +399,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
             mbar_init(&tempty[a], 128);
         }
         for (int a = 0; a < 4 * p.nbuf; ++a) mbar_init(&mbar_mask[a], 1);
+        mbar_init(bres_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -368,6 +423,78 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
         uint32_t it = 0;
         int ring_s = 0;        // it % S, kept as a running counter (no divisions)
         uint32_t ring_ph = 0;  // (it / S) & 1
+        if (p.bres) {
+            // this CTA's n tile is fixed (gridDim.x % n_tiles == 0): its B slice,
+            // every k-block of every operand pair, hi and lo, lands once
+            const int n0 = (int)(blockIdx.x % n_tiles) * p.BN;
+            if (elect_one()) {
+                uint32_t bytes = 0;
+                for (int o = 0; o < p.n_ops; ++o)
+                    bytes += 2u * ((p.op[o].K + BK - 1) / BK) *
+                             (p.op[o].b_mn ? nb_b * 32 * BK * 4 : p.BN * BK * 4);
+                mbar_expect_tx(bres_bar, bytes);
+                int kbg = 0;
+                for (int o = 0; o < p.n_ops; ++o) {
+                    const CUtensorMap *mb = o ? &mB1 : &mB0;
+                    const CUtensorMap *mbl = o ? &mBl1 : &mBl0;
+                    const int nkb = (p.op[o].K + BK - 1) / BK;
+                    for (int kb = 0; kb < nkb; ++kb, ++kbg) {
+                        uint8_t *sb = smem_raw + kbg * p.bres_kb;
+                        uint8_t *sbl = sb + p.bres_lo_off;
+                        if (p.op[o].b_mn) {
+                            for (int b = 0; b < nb_b; ++b) {
+                                tma_load_2d(mb, bres_bar, sb + b * 4096, n0 + 32 * b, kb * BK);
+                                tma_load_2d(mbl, bres_bar, sbl + b * 4096, n0 + 32 * b, kb * BK);
+                            }
+                        } else {
+                            tma_load_2d(mb, bres_bar, sb, kb * BK, n0);
+                            tma_load_2d(mbl, bres_bar, sbl, kb * BK, n0);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        // L2 prefetch cursor over this CTA's (tile, operand pair, k-block)
+        // sequence, pf_dist k-blocks ahead of the loads
+        int64_t pf_t = blockIdx.x;
+        int pf_o = 0, pf_kb = 0, pf_kb0 = 0, pf_nkb = 0;
+        TileCoord pf_tc = tile_of(p, pf_t < total_tiles ? pf_t : 0, n_tiles, m_tiles);
+        if (pf_t < total_tiles) kblocks(p, 0, pf_tc.z, pf_kb0, pf_nkb);
+        auto pf_step = [&]() {
+            if (pf_t >= total_tiles) return;
+            if (pf_kb < pf_nkb) {
+                const CUtensorMap *ma = pf_o ? &mA1 : &mA0;
+                const CUtensorMap *mb = pf_o ? &mB1 : &mB0;
+                const int k0 = (pf_kb0 + pf_kb) * BK;
+                if (lane == 0) {
+                    if (p.op[pf_o].a_mn) {
+                        for (int b = 0; b < 4; ++b) tma_prefetch_2d(ma, (int)(pf_tc.m0 + 32 * b), k0);
+                    } else {
+                        tma_prefetch_2d(ma, k0, (int)pf_tc.m0);
+                    }
+                    if (!p.bres && !p.b_presplit) {   // activations as B (weight gradient)
+                        if (p.op[pf_o].b_mn) {
+                            for (int b = 0; b < nb_b; ++b) tma_prefetch_2d(mb, pf_tc.n0 + 32 * b, k0);
+                        } else {
+                            tma_prefetch_2d(mb, k0, pf_tc.n0);
+                        }
+                    }
+                }
+            }
+            // advance
+            if (++pf_kb >= pf_nkb) {
+                pf_kb = 0;
+                if (++pf_o >= p.n_ops) {
+                    pf_o = 0;
+                    pf_t += gridDim.x;
+                    if (pf_t >= total_tiles) return;
+                    pf_tc = tile_of(p, pf_t, n_tiles, m_tiles);
+                }
+                kblocks(p, pf_o, pf_tc.z, pf_kb0, pf_nkb);
+            }
+        };
+        for (int d = 0; d < p.pf_dist; ++d) pf_step();
         for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
             const TileCoord tc = tile_of(p, t, n_tiles, m_tiles);
             for (int o = 0; o < p.n_ops; ++o) {
@@ -379,20 +506,23 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                 const uint32_t bbytes = p.op[o].b_mn ? nb_b * 32 * BK * 4 : p.BN * BK * 4;
                 for (int kb = kb0; kb < kb0 + nkb; ++kb, ++it) {
                     const int s = ring_s;
+                    if (p.pf_dist > 0) pf_step();
                     mbar_wait(&empty[s], ring_ph ^ 1);
                     if (++ring_s == S) { ring_s = 0; ring_ph ^= 1; }
                     const int k0 = kb * BK;
                     uint8_t *sa = smem + s * stage_bytes;
                     uint8_t *sb = sa + A_BYTES;
                     if (elect_one()) {
-                    mbar_expect_tx(&full[s], A_BYTES + bbytes * (p.b_presplit ? 2 : 1));
+                    mbar_expect_tx(&full[s], A_BYTES + (p.bres ? 0u : bbytes * (p.b_presplit ? 2 : 1)));
                     if (p.op[o].a_mn) {
                         for (int b = 0; b < 4; ++b)
                             tma_load_2d(ma, &full[s], sa + b * 4096, (int)(tc.m0 + 32 * b), k0);
                     } else {
                         tma_load_2d(ma, &full[s], sa, k0, (int)tc.m0);
                     }
-                    if (p.op[o].b_mn) {
+                    if (p.bres) {
+                        // B is resident
+                    } else if (p.op[o].b_mn) {
                         for (int b = 0; b < nb_b; ++b) {
                             tma_load_2d(mb, &full[s], sb + b * 4096, tc.n0 + 32 * b, k0);
                             if (p.b_presplit)
@@ -414,6 +544,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
         uint32_t it = 0, ti = 0;
         int ring_s = 0;
         uint32_t ring_ph = 0;
+        if (p.bres) mbar_wait(bres_bar, 0);
         for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++ti) {
             const TileCoord tc = tile_of(p, t, n_tiles, m_tiles);
             const uint32_t acc_buf = ti & 1;
@@ -421,6 +552,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t tmem_d = tmem_base + acc_buf * p.acc_stride;
             bool first = true;
+            int kbg = 0;   // global k-block index over the operand pairs (resident B)
             for (int o = 0; o < p.n_ops; ++o) {
                 int kb0, nkb;
                 kblocks(p, o, tc.z, kb0, nkb);
@@ -443,8 +575,10 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                     else mbar_wait(&full[s], ph);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     const uint32_t sa = smem_u32(smem + s * stage_bytes);
-                    const uint32_t sb = sa + A_BYTES;
-                    const uint32_t sa_lo = sa + HI_BYTES, sb_lo = sb + p.b_lo_off;
+                    const uint32_t sb = p.bres ? smem_u32(smem_raw) + (kbg + kb) * p.bres_kb
+                                               : sa + A_BYTES;
+                    const uint32_t sa_lo = sa + HI_BYTES;
+                    const uint32_t sb_lo = sb + (p.bres ? p.bres_lo_off : p.b_lo_off);
                     if (p.a_tmem) {
                         // A (= its TF32 truncation) and A_lo sit in TMEM slot s
                         mma_kblock_ts3(tmem_d, tmem_base + A_TMEM_COL + 64 * s,
@@ -477,11 +611,147 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                     first = false;
                     __syncwarp();
                 }
+                kbg += nkb;
             }
             if (lane == 0) mma_commit(&tfull[acc_buf]);
             __syncwarp();
         }
-    } else if (warp >= 4 && warp < 8) {
+    } else if (EPI >= 0 && warp >= 4 && warp < 8) {
+        // ------------------------------------------------ epilogue, compile-time
+        // variant: TMEM -> registers (the next 32-column chunk's load in flight
+        // while this one is processed) -> bias / ReLU / row scale / mask ->
+        // swizzled staging buffer -> TMA bulk store
+        constexpr bool HB = (EPI & EPI_BIAS) != 0, RL = (EPI & EPI_RELU) != 0;
+        constexpr bool RS = (EPI & EPI_RS) != 0, MK = (EPI & EPI_MASK) != 0;
+        // (a second group of epilogue warps taking every other chunk was
+        // measured slower once the operand feed, not the epilogue, bound
+        // these GEMMs: fwd0 57 -> 81 us with resident B)
+        const int q = warp & 3;
+        constexpr int G = 1, g = 0;
+        const int NB = p.nbuf;
+        const int nb_log = 31 - __clz(NB);
+        uint8_t *stg0 = smem + S * stage_bytes + SMEM_BARS + q * NB * EPI_BUF;
+        uint64_t *mbq = mbar_mask + q * NB;
+        uint32_t ti = 0, nst = 0;
+        // mask prefetch cursor (see the generic epilogue): D = NB - 2 chunks ahead
+        const int D = NB - 2;
+        int64_t pf_t = blockIdx.x;
+        int pf_c = g;
+        uint32_t pf_k = 0;
+        TileCoord pc = tile_of(p, pf_t < total_tiles ? pf_t : 0, n_tiles, m_tiles);
+        // first valid chunk of this group
+        while (pf_t < total_tiles && (pf_c * 32 >= p.BN || p.N - (pc.n0 + 32 * pf_c) <= 0)) {
+            pf_c = g;
+            pf_t += gridDim.x;
+            if (pf_t < total_tiles) pc = tile_of(p, pf_t, n_tiles, m_tiles);
+        }
+        auto pf_issue = [&]() -> bool {
+            if (pf_t >= total_tiles) return false;
+            if (lane == 0) {
+                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                uint64_t *bar = &mbq[pf_k & (NB - 1)];
+                mbar_expect_tx(bar, EPI_BUF);
+                tma_load_3d(&mM, bar, stg0 + (pf_k & (NB - 1)) * EPI_BUF, pc.n0 + 32 * pf_c,
+                            (int)(pc.m0 + 32 * q), 0);
+            }
+            ++pf_k;
+            while (true) {
+                pf_c += G;
+                if (pf_c * 32 >= p.BN) {
+                    pf_c = g;
+                    pf_t += gridDim.x;
+                    if (pf_t < total_tiles) pc = tile_of(p, pf_t, n_tiles, m_tiles);
+                }
+                if (pf_t >= total_tiles) break;
+                if (pf_c * 32 < p.BN && p.N - (pc.n0 + 32 * pf_c) > 0) break;
+            }
+            return true;
+        };
+        const int nch_max = (p.BN + 31) / 32;
+        for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++ti) {
+            const TileCoord tc = tile_of(p, t, n_tiles, m_tiles);
+            const uint32_t acc_buf = ti & 1;
+            const int64_t row = tc.m0 + 32 * q + lane;
+            float rs = 1.f;
+            if (RS && row < p.M) rs = __ldg(p.row_scale + row);
+            int nch = (p.N - tc.n0 + 31) / 32;
+            if (nch > nch_max) nch = nch_max;
+            mbar_wait(&tfull[acc_buf], (ti >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t tb = tmem_base + acc_buf * p.acc_stride + ((uint32_t)(32 * q) << 16);
+            uint32_t va[32], vb[32];
+            auto chunk = [&](const uint32_t (&v)[32], int c) {
+                const int c0 = 32 * c;
+                const int ncol = p.N - (tc.n0 + c0);   // > 0; may exceed 32
+                const uint32_t buf = nst & (NB - 1);
+                const uint32_t stg = smem_u32(stg0 + buf * EPI_BUF);
+                float4 mk[8];
+                if constexpr (MK) {
+                    while (pf_k <= nst + D && pf_issue()) {}
+                    mbar_wait(&mbq[buf], (nst >> nb_log) & 1);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(mk[j].x), "=f"(mk[j].y), "=f"(mk[j].z), "=f"(mk[j].w)
+                                     : "r"(stg + lane * 128 + 16 * (j ^ (lane & 7)))
+                                     : "memory");
+                } else {
+                    // the store NB chunks ago has finished reading this buffer
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                }
+                __syncwarp();
+                const float *brow = HB ? p.bias + tc.n0 + c0 : nullptr;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    float4 y = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                           __uint_as_float(v[4 * j + 2]),
+                                           __uint_as_float(v[4 * j + 3]));
+                    if constexpr (HB) {
+                        // columns >= N are clipped by the store; never read past the bias
+                        const float4 bb = 4 * j < ncol
+                            ? __ldg(reinterpret_cast<const float4 *>(brow) + j)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+                        y.x += bb.x; y.y += bb.y; y.z += bb.z; y.w += bb.w;
+                    }
+                    if constexpr (RL) {
+                        y.x = fmaxf(y.x, 0.f); y.y = fmaxf(y.y, 0.f);
+                        y.z = fmaxf(y.z, 0.f); y.w = fmaxf(y.w, 0.f);
+                    }
+                    if constexpr (RS) {
+                        y.x *= rs; y.y *= rs; y.z *= rs; y.w *= rs;
+                    }
+                    if constexpr (MK) {
+                        const float4 m = mk[j];
+                        y.x = m.x > 0.f ? y.x : 0.f; y.y = m.y > 0.f ? y.y : 0.f;
+                        y.z = m.z > 0.f ? y.z : 0.f; y.w = m.w > 0.f ? y.w : 0.f;
+                    }
+                    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                     stg + lane * 128 + 16 * (j ^ (lane & 7))),
+                                 "f"(y.x), "f"(y.y), "f"(y.z), "f"(y.w)
+                                 : "memory");
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0)
+                    tma_store_3d(&mC, stg0 + buf * EPI_BUF, tc.n0 + c0, (int)(tc.m0 + 32 * q), tc.z);
+                ++nst;
+            };
+            if (g < nch) tmem_ld32_issue(tb + 32 * g, va);
+            for (int c = g; c < nch; c += 2 * G) {
+                tmem_ld32_wait(va);
+                if (c + G < nch) tmem_ld32_issue(tb + 32 * (c + G), vb);
+                chunk(va, c);
+                if (c + G < nch) {
+                    tmem_ld32_wait(vb);
+                    if (c + 2 * G < nch) tmem_ld32_issue(tb + 32 * (c + 2 * G), va);
+                    chunk(vb, c + G);
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            mbar_arrive(&tempty[acc_buf]);
+        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    } else if (EPI < 0 && warp >= 4 && warp < 8) {
         // ------------------------------------------------ epilogue
         // Warp q owns TMEM lanes 32q..32q+31 = tile rows; thread = one output
         // row.  Each 32-column chunk goes TMEM -> 32 registers -> bias / ReLU
@@ -864,6 +1134,46 @@ bool make_map_c(CUtensorMap *m, float *C, int64_t M, int N, int64_t ldc, int64_t
                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+typedef void (*KernelFn)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
+                         const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
+                         const Params);
+
+template <int EPI>
+KernelFn prepared() {
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<EPI>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
+        if (e != cudaSuccess) {
+            cg_cuda_fail(e, "cudaFuncSetAttribute(k_gemm_tc)");
+            return nullptr;
+        }
+        attr_set = true;
+    }
+    return k_gemm_tc<EPI>;
+}
+
+// The variants the training epoch uses: weight gradients and SAGE's second
+// input-gradient term (none), the last layer's transform (bias), SAGE hidden
+// layers (bias + ReLU), GCN input gradients (row scale), GCN hidden layers
+// (bias + ReLU + row scale), and the ReLU-backward masked input gradient.
+bool instantiated(int epi) {
+    return epi == 0 || epi == EPI_BIAS || epi == (EPI_BIAS | EPI_RELU) || epi == EPI_RS ||
+           epi == (EPI_BIAS | EPI_RELU | EPI_RS) || epi == EPI_MASK;
+}
+
+KernelFn kernel_for(int epi) {
+    switch (epi) {
+        case 0: return prepared<0>();
+        case EPI_BIAS: return prepared<EPI_BIAS>();
+        case EPI_BIAS | EPI_RELU: return prepared<EPI_BIAS | EPI_RELU>();
+        case EPI_RS: return prepared<EPI_RS>();
+        case EPI_BIAS | EPI_RELU | EPI_RS: return prepared<EPI_BIAS | EPI_RELU | EPI_RS>();
+        case EPI_MASK: return prepared<EPI_MASK>();
+        default: return prepared<EPI_GENERIC>();
+    }
+}
+
 int launch(const Params &p0, const CUtensorMap &a0, const CUtensorMap &b0, const CUtensorMap &a1,
            const CUtensorMap &b1, const CUtensorMap &bl0, const CUtensorMap &bl1, int grid_z,
            cudaStream_t st) {
@@ -898,16 +1208,52 @@ int launch(const Params &p0, const CUtensorMap &a0, const CUtensorMap &b0, const
         p.b_lo_off = p.hi_bytes;
         p.acc_stride = BN_MAX;
     }
+    // resident B: a weight operand (pre-split hi / lo, no split-K) whose whole
+    // CTA slice fits beside the ring is loaded once per CTA; each CTA then
+    // keeps one n tile (grid a multiple of the n-tile count) and streams only
+    // A -- the per-tile B re-reads from L2 were the short-K GEMMs' bound
+    static const bool no_bres = getenv("CG_GEMM_NO_BRES") != nullptr;   // A/B knob
+    p.bres = 0;
+    p.ring_off = 0;
+    {
+        int total_kb = 0;
+        for (int o = 0; o < p.n_ops; ++o) total_kb += (p.op[o].K + BK - 1) / BK;
+        const int bres_bytes = 2 * total_kb * b_bytes;
+        const int n_tiles_ = (p.N + p.BN - 1) / p.BN;
+        if (!no_bres && p.a_tmem && p.b_presplit && p.k_chunk == 0 && grid_z == 1 &&
+            bres_bytes <= 144 * 1024 && n_tiles_ <= 148) {
+            p.bres = 1;
+            p.ring_off = bres_bytes;
+            p.bres_kb = b_bytes;
+            p.bres_lo_off = total_kb * b_bytes;
+            p.stage_bytes = A_BYTES;   // the ring carries A only
+        }
+    }
+    static const int env_pf = getenv("CG_GEMM_PF") ? atoi(getenv("CG_GEMM_PF")) : -1;
+    // measured (C2 shapes): 2 k-blocks ahead helps the A-streaming resident-B
+    // GEMMs (fwd0 56.7 -> 53.3 us, fwd2 41.1 -> 37.7 us) and costs the others
+    // (fwd1 100.7 -> 109.9 us), which stay without
+    p.pf_dist = env_pf >= 0 ? env_pf : (p.bres ? 2 : 0);   // CG_GEMM_PF: A/B knob
     const int stage_bytes = p.stage_bytes;
+    // the compile-time epilogue variant (TMA-store path, 16-byte bias rows,
+    // N % 4 == 0); anything else takes the generic epilogue
+    static const bool no_fast = getenv("CG_GEMM_GENERIC_EPI") != nullptr;  // A/B knob
+    int epi = EPI_GENERIC;
+    if (!no_fast && !dbg && p.tma_store && (!p.mask || p.tma_mask) && !(p.N % 4) &&
+        (!p.bias || !((uintptr_t)p.bias % 16)))
+        epi = (p.bias ? EPI_BIAS : 0) | (p.relu ? EPI_RELU : 0) | (p.row_scale ? EPI_RS : 0) |
+              (p.mask ? EPI_MASK : 0);
+    if (!instantiated(epi)) epi = EPI_GENERIC;
     // masked epilogues prefetch their mask tiles NB - 2 chunks ahead: 4 staging
     // buffers per warp, 8 when K is short (<= 2 k-blocks: the epilogue, not the
-    // MMA, is then the critical path and 2 operand stages suffice)
+    // MMA, is then the critical path and 2 operand stages suffice) and one
+    // epilogue group drains the tile
     static const int env_nbuf = getenv("CG_GEMM_MASK_NBUF") ? atoi(getenv("CG_GEMM_MASK_NBUF")) : 0;
     const bool short_k = p.n_ops == 1 && p.op[0].K <= 2 * BK;
     const bool env_ok = env_nbuf >= 4 && env_nbuf <= 8 && !(env_nbuf & (env_nbuf - 1));  // 4 or 8
     p.nbuf = p.tma_mask ? (env_ok ? env_nbuf : (short_k ? 8 : 4)) : 2;
     const int smem_fixed = SMEM_BARS + 4 * p.nbuf * EPI_BUF;
-    int stages = (SMEM_LIMIT - smem_fixed) / stage_bytes;
+    int stages = (SMEM_LIMIT - smem_fixed - p.ring_off) / stage_bytes;
     static const int env_stages = getenv("CG_GEMM_STAGES") ? atoi(getenv("CG_GEMM_STAGES")) : 0;
     int cap = env_stages > 0 ? env_stages : 6;   // experiment knob
     if (p.a_tmem && cap > 4) cap = 4;            // TMEM: 2 x 128 accumulator + 4 x 64 A columns
@@ -916,14 +1262,9 @@ int launch(const Params &p0, const CUtensorMap &a0, const CUtensorMap &b0, const
         cg_set_error("k_gemm_tc: stage does not fit shared memory");
         return -1;
     }
-    const size_t smem = (size_t)p.stages * stage_bytes + smem_fixed;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             SMEM_LIMIT);
-        if (e != cudaSuccess) return cg_cuda_fail(e, "cudaFuncSetAttribute(k_gemm_tc)");
-        attr_set = true;
-    }
+    const size_t smem = (size_t)p.ring_off + (size_t)p.stages * stage_bytes + smem_fixed;
+    KernelFn kern = kernel_for(epi);
+    if (!kern) return -1;
     static int n_sm = 0;
     if (!n_sm) {
         int dev = 0;
@@ -932,9 +1273,12 @@ int launch(const Params &p0, const CUtensorMap &a0, const CUtensorMap &b0, const
         if (n_sm <= 0) n_sm = 148;
     }
     const int64_t tiles = (int64_t)((p.N + p.BN - 1) / p.BN) * ((p.M + BM - 1) / BM) * grid_z;
-    const unsigned grid = (unsigned)(tiles < n_sm ? tiles : n_sm);   // persistent
-    cgpdl::launch(k_gemm_tc, dim3(grid), dim3(THREADS), smem, st, a0, b0, a1, b1, bl0, bl1, mc, mm,
-                  p);
+    unsigned grid = (unsigned)(tiles < n_sm ? tiles : n_sm);   // persistent
+    if (p.bres) {   // every CTA keeps one n tile
+        const unsigned nt = (unsigned)((p.N + p.BN - 1) / p.BN);
+        grid = grid / nt * nt;
+    }
+    cgpdl::launch(kern, dim3(grid), dim3(THREADS), smem, st, a0, b0, a1, b1, bl0, bl1, mc, mm, p);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 1 : cg_cuda_fail(e, "k_gemm_tc");
 }

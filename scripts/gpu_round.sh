@@ -24,17 +24,17 @@ fi
 
 # launch list (cold-cache, serialised): shares per kernel, not absolutes
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-  --log-file "$OUT/launches.csv" python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
+  --log-file "$OUT/launches.csv" python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-exchange \
   > "$OUT/launches_bench.log" 2>&1
 python tests/launch_breakdown.py "$OUT/launches.csv" > "$OUT/launches_summary.txt" 2>&1
 
 # one full capture of the SpMM: one epoch worth of launches after warm-up
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_spmm -s 24 -c 8 \
-  -o "$OUT/prof_spmm" python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
+  -o "$OUT/prof_spmm" python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-exchange \
   > "$OUT/prof_spmm.log" 2>&1
 if [ -z "${SKIP_GEMM_PROF:-}" ]; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gemm_tc -s 18 -c 3 \
-    -o "$OUT/prof_gemm" python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
+    -o "$OUT/prof_gemm" python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-exchange \
     > "$OUT/prof_gemm.log" 2>&1
 fi
 echo done > "$OUT/DONE"
