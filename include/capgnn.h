@@ -122,6 +122,15 @@ int cg_spmm(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col,
             const float *scale, const float *addend, int64_t ld_add,
             const float *mask, int64_t ld_mask, float *out, int64_t ldo, int64_t nnz,
             void *stream);
+/* The same aggregation with the ReLU-backward mask given as BITS: bit j of
+ * word w of row r (mask_bits[r * ld_mask_bits + w]) stands for column
+ * 32 w + j being > 0 -- the pattern cg_gemm_mb's bits_out writes for a
+ * ReLU layer's output, 1/32 of the fp32 mask's bytes.  F % 32 == 0.       */
+int cg_spmm_mb(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col,
+               int64_t n_direct, const int32_t *halo_row, const float *X, int64_t ldx,
+               const float *scale, const float *addend, int64_t ld_add,
+               const uint32_t *mask_bits, int64_t ld_mask_bits, float *out, int64_t ldo,
+               int64_t nnz, void *stream);
 
 /* ---- K5: dense transform ---------------------------------------------- */
 /* C[m, n] = epi( sum_k A1[m,k] B1[k,n] + sum_k A2[m,k] B2[k,n] )  (A2 optional)
@@ -137,6 +146,17 @@ int cg_gemm(int64_t M, int N, int K1, const float *A1, int64_t lda1,
             int trans_b, const float *bias, int relu, const float *row_scale,
             const float *mask, int64_t ldm, float *C, int64_t ldc, int mode,
             const float *B1_lo, const float *B2_lo, void *stream);
+/* cg_gemm (tcgen05 modes 1 / 2) with the ReLU-backward mask as bits
+ * (mask_bits, format as for cg_spmm_mb; may be NULL) and, for a ReLU layer,
+ * the output's > 0 pattern written as bits (bits_out; may be NULL) -- the
+ * masks the backward pass reads, at 1/32 of the fp32 bytes.  Bits need
+ * N % 32 == 0 with N <= 128 or N % 128 == 0.                              */
+int cg_gemm_mb(int64_t M, int N, int K1, const float *A1, int64_t lda1,
+               const float *B1, int K2, const float *A2, int64_t lda2, const float *B2,
+               int trans_b, const float *bias, int relu, const float *row_scale,
+               const uint32_t *mask_bits, int64_t ld_mask_bits, uint32_t *bits_out,
+               int64_t ld_bits_out, float *C, int64_t ldc, int mode, const float *B1_lo,
+               const float *B2_lo, void *stream);
 /* hi[i] = x[i] with the low 13 mantissa bits cleared (a TF32 value),
  * lo[i] = x[i] - hi[i] (exact).                                           */
 int cg_split_tf32(int64_t n, const float *x, float *hi, float *lo, void *stream);

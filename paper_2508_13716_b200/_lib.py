@@ -55,6 +55,9 @@ SIGNATURES = {
     "cg_flag_signal": [P, C.c_uint32, P],
     "cg_flag_wait": [P, INT, INT, C.c_uint32, P],
     "cg_spmm": [I64, INT, P, P, I64, P, P, I64, P, P, I64, P, I64, P, I64, I64, P],
+    "cg_spmm_mb": [I64, INT, P, P, I64, P, P, I64, P, P, I64, P, I64, P, I64, I64, P],
+    "cg_gemm_mb": [I64, INT, INT, P, I64, P, INT, P, I64, P, INT, P, INT, P, P, I64, P, I64, P,
+                   I64, INT, P, P, P],
     "cg_gemm": [I64, INT, INT, P, I64, P, INT, P, I64, P, INT, P, INT, P, P, I64, P, I64, INT,
                 P, P, P],
     "cg_split_tf32": [I64, P, P, P, P],
@@ -122,7 +125,7 @@ def lib():
 # total is the bench's "gpu_launches" evidence
 KERNEL_ENTRY = {"cg_hash_features", "cg_hash_labels", "cg_scale_rows", "cg_scale_rows_to",
                 "cg_copy_rows", "cg_copy_rows_bounded", "cg_copy_rows_sel",
-                "cg_spmm", "cg_gemm", "cg_wgrad", "cg_colsum", "cg_softmax_ce", "cg_adam",
+                "cg_spmm", "cg_spmm_mb", "cg_gemm", "cg_gemm_mb", "cg_wgrad", "cg_colsum", "cg_softmax_ce", "cg_adam",
                 "cg_split_tf32", "cg_split_tf32_t",
                 "cg_plan_frozen", "cg_set_epoch"}
 launches = {"total": 0}

@@ -21,7 +21,9 @@ extern int cg_cuda_fail(cudaError_t e, const char *what);
 int cg_gemm_tc(int64_t M, int N, int K1, const float *A1, int64_t lda1, const float *B1, int K2,
                const float *A2, int64_t lda2, const float *B2, int trans_b, const float *bias,
                int relu, const float *row_scale, const float *mask, int64_t ldm, float *C,
-               int64_t ldc, int mode, const float *B1_lo, const float *B2_lo, cudaStream_t st);
+               int64_t ldc, int mode, const float *B1_lo, const float *B2_lo,
+               const uint32_t *mbits, int64_t ld_mbits, uint32_t *bits_out, int64_t ld_bits_out,
+               cudaStream_t st);
 int cg_wgrad_tc(int64_t M, int K, int N, const float *A, int64_t lda, const float *D, int64_t ldd,
                 float *ws, int64_t chunk, int64_t n_chunks, int mode, float *bws,
                 cudaStream_t st);
@@ -191,14 +193,29 @@ int cg_gemm(int64_t M, int N, int K1, const float *A1, int64_t lda1, const float
     if (M == 0 || N == 0) return 0;
     if (mode != 0)
         return cg_gemm_tc(M, N, K1, A1, lda1, B1, K2, A2, lda2, B2, trans_b, bias, relu,
-                          row_scale, mask, ldm, C, ldc, mode, B1_lo, B2_lo,
-                          (cudaStream_t)stream);
+                          row_scale, mask, ldm, C, ldc, mode, B1_lo, B2_lo, nullptr, 0, nullptr,
+                          0, (cudaStream_t)stream);
     dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN));
     k_gemm<<<grid, NT, 0, (cudaStream_t)stream>>>(M, N, K1, A1, lda1, B1, K2, A2, lda2, B2,
                                                  trans_b, bias, relu, row_scale, mask, ldm,
                                                  C, ldc);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 1 : cg_cuda_fail(e, "k_gemm");
+}
+
+int cg_gemm_mb(int64_t M, int N, int K1, const float *A1, int64_t lda1, const float *B1, int K2,
+               const float *A2, int64_t lda2, const float *B2, int trans_b, const float *bias,
+               int relu, const float *row_scale, const uint32_t *mask_bits, int64_t ld_mask_bits,
+               uint32_t *bits_out, int64_t ld_bits_out, float *C, int64_t ldc, int mode,
+               const float *B1_lo, const float *B2_lo, void *stream) {
+    if (M == 0 || N == 0) return 0;
+    if (mode != 1 && mode != 2) {
+        cg_set_error("cg_gemm_mb: mask bits need a tcgen05 mode (1 or 2)");
+        return -1;
+    }
+    return cg_gemm_tc(M, N, K1, A1, lda1, B1, K2, A2, lda2, B2, trans_b, bias, relu, row_scale,
+                      nullptr, 0, C, ldc, mode, B1_lo, B2_lo, mask_bits, ld_mask_bits, bits_out,
+                      ld_bits_out, (cudaStream_t)stream);
 }
 
 int64_t cg_wgrad_workspace(int64_t M, int K, int N) {

@@ -85,6 +85,10 @@ struct Params {
     int bres_kb;     // bytes per resident k-block of B (hi; lo at bres_lo_off)
     int bres_lo_off;
     int pf_dist;     // k-blocks the L2 prefetch cursor runs ahead of the TMA loads
+    const uint32_t *mbits;   // ReLU-backward mask as bits (bit j of word w of a row =
+    int64_t ld_mbits;        //   column 32 w + j > 0), words per row
+    uint32_t *bits_out;      // ReLU layers: the output's > 0 pattern, same format
+    int64_t ld_bits_out;
     float *bws;      // weight gradient only: per (chunk, splitter warp) column sums
                      // of the MN-major B operand (= the bias gradient partials)
     int dbg;         // diagnostics only (CG_GEMM_DBG, wrong results): 1 = splitter
@@ -315,7 +319,8 @@ __device__ __forceinline__ void tmem_ld32_wait(uint32_t (&r)[32]) {
 // ReLU, bit 2 row scale, bit 3 ReLU-backward mask (TMA-loaded).  EPI_GENERIC
 // keeps every operand a runtime switch (direct stores, unaligned shapes,
 // the diagnostics knobs).
-constexpr int EPI_BIAS = 1, EPI_RELU = 2, EPI_RS = 4, EPI_MASK = 8, EPI_GENERIC = -1;
+constexpr int EPI_BIAS = 1, EPI_RELU = 2, EPI_RS = 4, EPI_MASK = 8, EPI_MBITS = 16,
+              EPI_GENERIC = -1;
 
 // Tile t of the persistent schedule -> (m tile, n tile, split-K chunk);
 // consecutive t share the m tile so concurrently running CTAs reuse the A
@@ -623,6 +628,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
         // swizzled staging buffer -> TMA bulk store
         constexpr bool HB = (EPI & EPI_BIAS) != 0, RL = (EPI & EPI_RELU) != 0;
         constexpr bool RS = (EPI & EPI_RS) != 0, MK = (EPI & EPI_MASK) != 0;
+        constexpr bool MB = (EPI & EPI_MBITS) != 0;
         // (a second group of epilogue warps taking every other chunk was
         // measured slower once the operand feed, not the epilogue, bound
         // these GEMMs: fwd0 57 -> 81 us with resident B)
@@ -701,6 +707,11 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                 }
                 __syncwarp();
                 const float *brow = HB ? p.bias + tc.n0 + c0 : nullptr;
+                const bool row_ok = row < p.M;
+                uint32_t mw = 0, bw = 0;   // mask bits in, ReLU bits out (32 columns)
+                if constexpr (MB) {
+                    if (row_ok) mw = __ldg(p.mbits + row * p.ld_mbits + ((tc.n0 + c0) >> 5));
+                }
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     float4 y = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
@@ -725,10 +736,26 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                         y.x = m.x > 0.f ? y.x : 0.f; y.y = m.y > 0.f ? y.y : 0.f;
                         y.z = m.z > 0.f ? y.z : 0.f; y.w = m.w > 0.f ? y.w : 0.f;
                     }
+                    if constexpr (MB) {
+                        const uint32_t b = mw >> (4 * j);
+                        y.x = (b & 1u) ? y.x : 0.f; y.y = (b & 2u) ? y.y : 0.f;
+                        y.z = (b & 4u) ? y.z : 0.f; y.w = (b & 8u) ? y.w : 0.f;
+                    }
+                    if constexpr (RL) {
+                        bw |= ((y.x > 0.f ? 1u : 0u) | (y.y > 0.f ? 2u : 0u) |
+                               (y.z > 0.f ? 4u : 0u) | (y.w > 0.f ? 8u : 0u)) << (4 * j);
+                    }
                     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
                                      stg + lane * 128 + 16 * (j ^ (lane & 7))),
                                  "f"(y.x), "f"(y.y), "f"(y.z), "f"(y.w)
                                  : "memory");
+                }
+                if constexpr (RL) {
+                    // the > 0 pattern of the stored values (columns >= N clip to 0)
+                    if (p.bits_out && row_ok) {
+                        if (ncol < 32) bw &= (1u << ncol) - 1u;
+                        p.bits_out[row * p.ld_bits_out + ((tc.n0 + c0) >> 5)] = bw;
+                    }
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
@@ -1159,7 +1186,7 @@ KernelFn prepared() {
 // (bias + ReLU + row scale), and the ReLU-backward masked input gradient.
 bool instantiated(int epi) {
     return epi == 0 || epi == EPI_BIAS || epi == (EPI_BIAS | EPI_RELU) || epi == EPI_RS ||
-           epi == (EPI_BIAS | EPI_RELU | EPI_RS) || epi == EPI_MASK;
+           epi == (EPI_BIAS | EPI_RELU | EPI_RS) || epi == EPI_MASK || epi == EPI_MBITS;
 }
 
 KernelFn kernel_for(int epi) {
@@ -1170,6 +1197,7 @@ KernelFn kernel_for(int epi) {
         case EPI_RS: return prepared<EPI_RS>();
         case EPI_BIAS | EPI_RELU | EPI_RS: return prepared<EPI_BIAS | EPI_RELU | EPI_RS>();
         case EPI_MASK: return prepared<EPI_MASK>();
+        case EPI_MBITS: return prepared<EPI_MBITS>();
         default: return prepared<EPI_GENERIC>();
     }
 }
@@ -1242,8 +1270,14 @@ int launch(const Params &p0, const CUtensorMap &a0, const CUtensorMap &b0, const
     if (!no_fast && !dbg && p.tma_store && (!p.mask || p.tma_mask) && !(p.N % 4) &&
         (!p.bias || !((uintptr_t)p.bias % 16)))
         epi = (p.bias ? EPI_BIAS : 0) | (p.relu ? EPI_RELU : 0) | (p.row_scale ? EPI_RS : 0) |
-              (p.mask ? EPI_MASK : 0);
+              (p.mask ? EPI_MASK : 0) | (p.mbits ? EPI_MBITS : 0);
     if (!instantiated(epi)) epi = EPI_GENERIC;
+    if ((p.mbits || p.bits_out) &&
+        (epi == EPI_GENERIC || (p.BN % 32) || (p.bits_out && !p.relu))) {
+        cg_set_error("k_gemm_tc: mask bits need the TMA-store epilogue, 32-column tiles "
+                     "(N % 32 == 0 and N <= 128 or N % 128 == 0) and, for bits out, ReLU");
+        return -1;
+    }
     // masked epilogues prefetch their mask tiles NB - 2 chunks ahead: 4 staging
     // buffers per warp, 8 when K is short (<= 2 k-blocks: the epilogue, not the
     // MMA, is then the critical path and 2 operand stages suffice) and one
@@ -1298,7 +1332,9 @@ inline int bn_for(int N, bool split3) {
 int cg_gemm_tc(int64_t M, int N, int K1, const float *A1, int64_t lda1, const float *B1, int K2,
                const float *A2, int64_t lda2, const float *B2, int trans_b, const float *bias,
                int relu, const float *row_scale, const float *mask, int64_t ldm, float *C,
-               int64_t ldc, int mode, const float *B1_lo, const float *B2_lo, cudaStream_t st) {
+               int64_t ldc, int mode, const float *B1_lo, const float *B2_lo,
+               const uint32_t *mbits, int64_t ld_mbits, uint32_t *bits_out, int64_t ld_bits_out,
+               cudaStream_t st) {
     using namespace tc;
     if (mode != 1 && mode != 2) {
         cg_set_error("cg_gemm: unknown mode");
@@ -1319,6 +1355,10 @@ int cg_gemm_tc(int64_t M, int N, int K1, const float *A1, int64_t lda1, const fl
     p.row_scale = row_scale;
     p.mask = mask;
     p.ldm = ldm;
+    p.mbits = mbits;
+    p.ld_mbits = ld_mbits;
+    p.bits_out = bits_out;
+    p.ld_bits_out = ld_bits_out;
     p.C = C;
     p.ldc = ldc;
     p.k_chunk = 0;

@@ -23,7 +23,8 @@ extern void cg_set_error(const std::string &msg);
 int cg_spmm_async(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col,
                   int64_t n_direct, const int32_t *halo_row, const float *X, int64_t ldx,
                   const float *scale, const float *addend, int64_t ld_add, const float *mask,
-                  int64_t ld_mask, float *out, int64_t ldo, cudaStream_t st);
+                  int64_t ld_mask, const uint32_t *mbits, int64_t ld_mbits, float *out,
+                  int64_t ldo, cudaStream_t st);
 extern int cg_cuda_fail(cudaError_t e, const char *what);
 
 #define CG_CHECK_LAUNCH(name)                                   \
@@ -154,13 +155,20 @@ k_spmm(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
        const int32_t *__restrict__ col, int64_t n_direct, const int32_t *__restrict__ halo_row,
        const float *__restrict__ X, int64_t ldx, const float *__restrict__ scale,
        const float *__restrict__ addend, int64_t ld_add, const float *__restrict__ mask,
-       int64_t ld_mask, float *__restrict__ out, int64_t ldo) {
+       int64_t ld_mask, const uint32_t *__restrict__ mbits, int64_t ld_mbits,
+       float *__restrict__ out, int64_t ldo, int flags) {
     pdl_entry();
     constexpr int UNR = (NCH == 1) ? SPMM_UNR1 : SPMM_UNR2;   // rows in flight per lane
     uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    uint64_t pol_first;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+    if (flags & 4)   // CG_SPMM_FLAGS bit 2: gathered rows at the default priority
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    else
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    uint64_t pol_first;   // bit 0: outputs evict_first (else evict_normal)
+    if (flags & 1)
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+    else
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_first));
     const int lane = threadIdx.x & (G - 1);
     const unsigned gmask = (G == 32) ? 0xffffffffu
                                      : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
@@ -255,6 +263,11 @@ k_spmm(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
                 o.y = m.y > 0.f ? o.y : 0.f;
                 o.z = m.z > 0.f ? o.z : 0.f;
                 o.w = m.w > 0.f ? o.w : 0.f;
+            }
+            if (mbits) {   // the same mask as bits: column 4 ch + i is bit (4 ch + i) % 32
+                const uint32_t b = mbits[r * ld_mbits + (ch >> 3)] >> (4 * (ch & 7));
+                o.x = (b & 1u) ? o.x : 0.f; o.y = (b & 2u) ? o.y : 0.f;
+                o.z = (b & 4u) ? o.z : 0.f; o.w = (b & 8u) ? o.w : 0.f;
             }
             // written once, never re-read by this launch: evict_first (see
             // spmm_async.cu), so the output does not displace gathered rows
@@ -951,10 +964,11 @@ int cg_copy_rows(int64_t n, int F, const int32_t *src_id, const int32_t *src_row
                                 stream);
 }
 
-int cg_spmm(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col, int64_t n_direct,
-            const int32_t *halo_row, const float *X, int64_t ldx, const float *scale,
-            const float *addend, int64_t ld_add, const float *mask, int64_t ld_mask, float *out,
-            int64_t ldo, int64_t nnz, void *stream) {
+static int spmm_impl(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col,
+                     int64_t n_direct, const int32_t *halo_row, const float *X, int64_t ldx,
+                     const float *scale, const float *addend, int64_t ld_add, const float *mask,
+                     int64_t ld_mask, const uint32_t *mbits, int64_t ld_mbits, float *out,
+                     int64_t ldo, int64_t nnz, void *stream) {
     if (n_rows == 0) return 0;
     if (F % 4 || ldx % 4 || ldo % 4 || (addend && ld_add % 4) || (mask && ld_mask % 4) ||
         ((uintptr_t)X % 16) || ((uintptr_t)out % 16)) {
@@ -974,10 +988,15 @@ int cg_spmm(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col, in
     static const int async_env = getenv("CG_SPMM_ASYNC") ? atoi(getenv("CG_SPMM_ASYNC")) : -1;
     const bool sparse = nnz >= 0 && nnz < 64 * n_rows;
     const bool fits_l2 = n_rows * (int64_t)F * 4 <= (int64_t)96 << 20;
-    // (F <= 48 with rows in L2: 4-lane streams, C2 40-wide 0.055 vs 0.061 ms)
+    // (F <= 48: 4-lane streams, C2 40-wide 0.055 vs 0.061 ms; on C4's
+    // products-shaped CSR (26 edges/row, 4.9M source rows, beyond L2) the
+    // ring also wins for F <= 48 -- the epoch's 48-wide backward 3.42 ->
+    // 2.31 ms -- while the 100-wide forward, DRAM-bound on 400-byte rows,
+    // stays faster on the register kernel in the epoch (5.57 vs 5.79 ms with
+    // the halo_row indirection; profiles/r02/spmm_c4.txt, r02/c4/)
     const bool use_async =
         async_env == 1 ||
-        (async_env != 0 && sparse && (F > 128 || (fits_l2 && (F > 64 || F <= 48))));
+        (async_env != 0 && sparse && (F > 128 || F <= 48 || (fits_l2 && F > 64)));
     if (use_async) {
         // Wide rows whose 128-column slice fits L2 are aggregated one slice at
         // a time: each pass re-reads the CSR indices but finds most gathered
@@ -992,7 +1011,9 @@ int cg_spmm(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col, in
             const int w = F - c0 < W ? F - c0 : W;
             const int rc = cg_spmm_async(n_rows, w, rowptr, col, n_direct, halo_row, X + c0, ldx,
                                          scale, addend ? addend + c0 : nullptr, ld_add,
-                                         mask ? mask + c0 : nullptr, ld_mask, out + c0, ldo, st);
+                                         mask ? mask + c0 : nullptr, ld_mask,
+                                         mbits ? mbits + c0 / 32 : nullptr, ld_mbits, out + c0,
+                                         ldo, st);
             if (rc < 0) return rc;
             if (rc == 0) { total = 0; break; }   // not applicable: fall back whole
             total += rc;
@@ -1001,6 +1022,7 @@ int cg_spmm(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col, in
     }
     const int nchunk = F / 4;
     const int threads = 256;
+    static const int reg_flags = getenv("CG_SPMM_FLAGS") ? atoi(getenv("CG_SPMM_FLAGS")) : 1;
 #define CG_SPMM_LAUNCH(G, NCH)                                                              \
     do {                                                                                    \
         static int blocks_per_sm = 0;                                                       \
@@ -1012,7 +1034,8 @@ int cg_spmm(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col, in
         cgpdl::launch(k_spmm<G, NCH>,                                                        \
                       dim3(grid_for(n_rows * G, threads, n_sms() * blocks_per_sm)),          \
                       dim3(threads), 0, st, n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, \
-                      scale, addend, ld_add, mask, ld_mask, out, ldo);                       \
+                      scale, addend, ld_add, mask, ld_mask, mbits, ld_mbits, out, ldo,       \
+                      reg_flags);                                                            \
     } while (0)
     if (nchunk <= 8) CG_SPMM_LAUNCH(8, 1);
     else if (nchunk <= 16) CG_SPMM_LAUNCH(16, 1);
@@ -1028,6 +1051,27 @@ int cg_spmm(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col, in
 #undef CG_SPMM_LAUNCH
     CG_CHECK_LAUNCH("k_spmm");
     return 1;
+}
+
+int cg_spmm(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col, int64_t n_direct,
+            const int32_t *halo_row, const float *X, int64_t ldx, const float *scale,
+            const float *addend, int64_t ld_add, const float *mask, int64_t ld_mask, float *out,
+            int64_t ldo, int64_t nnz, void *stream) {
+    return spmm_impl(n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, scale, addend, ld_add,
+                     mask, ld_mask, nullptr, 0, out, ldo, nnz, stream);
+}
+
+int cg_spmm_mb(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col,
+               int64_t n_direct, const int32_t *halo_row, const float *X, int64_t ldx,
+               const float *scale, const float *addend, int64_t ld_add,
+               const uint32_t *mask_bits, int64_t ld_mask_bits, float *out, int64_t ldo,
+               int64_t nnz, void *stream) {
+    if (mask_bits && (F % 32)) {
+        cg_set_error("cg_spmm_mb: mask bits need F % 32 == 0");
+        return -1;
+    }
+    return spmm_impl(n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, scale, addend, ld_add,
+                     nullptr, 0, mask_bits, ld_mask_bits, out, ldo, nnz, stream);
 }
 
 int cg_scale_rows(float *X, int64_t ld, int64_t n_rows, int F, const float *scale,

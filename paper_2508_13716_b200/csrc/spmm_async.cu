@@ -73,7 +73,8 @@ k_spmm_cpa(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
            const int32_t *__restrict__ col, int64_t n_direct, const int32_t *__restrict__ halo_row,
            const float *__restrict__ X, int64_t ldx, const float *__restrict__ scale,
            const float *__restrict__ addend, int64_t ld_add, const float *__restrict__ mask,
-           int64_t ld_mask, float *__restrict__ out, int64_t ldo, int64_t rows_per_warp,
+           int64_t ld_mask, const uint32_t *__restrict__ mbits, int64_t ld_mbits,
+           float *__restrict__ out, int64_t ldo, int64_t rows_per_warp,
            int flags) {
     extern __shared__ __align__(16) float4 ring_all[];
     pdl_entry();
@@ -148,6 +149,7 @@ k_spmm_cpa(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
     float sc = sc_at(rwin + lane), sc_n = sc_at(rwin + G + lane);
     int32_t row_end_e = __shfl_sync(gmask, rp, 0, G);
     float4 acc[NCH], pa[NCH], pm[NCH];
+    uint32_t pb[NCH];   // ReLU-backward mask bits (4 per chunk), when given as bits
 #pragma unroll
     for (int c = 0; c < NCH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
     auto open_row = [&]() {   // the epilogue operands of `row`, loaded early
@@ -160,6 +162,7 @@ k_spmm_cpa(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
                     pa[c] = reinterpret_cast<const float4 *>(addend + (int64_t)row * ld_add)[ch];
                 if (mask)
                     pm[c] = reinterpret_cast<const float4 *>(mask + (int64_t)row * ld_mask)[ch];
+                if (mbits) pb[c] = mbits[(int64_t)row * ld_mbits + (ch >> 3)] >> (4 * (ch & 7));
             }
         }
     };
@@ -180,6 +183,10 @@ k_spmm_cpa(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
             if (EPI && mask) {
                 o.x = pm[c].x > 0.f ? o.x : 0.f; o.y = pm[c].y > 0.f ? o.y : 0.f;
                 o.z = pm[c].z > 0.f ? o.z : 0.f; o.w = pm[c].w > 0.f ? o.w : 0.f;
+            }
+            if (EPI && mbits) {
+                o.x = (pb[c] & 1u) ? o.x : 0.f; o.y = (pb[c] & 2u) ? o.y : 0.f;
+                o.z = (pb[c] & 4u) ? o.z : 0.f; o.w = (pb[c] & 8u) ? o.w : 0.f;
             }
             st_out(reinterpret_cast<float4 *>(out + (int64_t)row * ldo) + ch, o, flags,
                    pol_first);
@@ -224,7 +231,8 @@ k_spmm_cpa(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
 template <int G, int NCH, int S, bool EPI>
 int launch_epi(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col, int64_t n_direct,
            const int32_t *halo_row, const float *X, int64_t ldx, const float *scale,
-           const float *addend, int64_t ld_add, const float *mask, int64_t ld_mask, float *out,
+           const float *addend, int64_t ld_add, const float *mask, int64_t ld_mask,
+           const uint32_t *mbits, int64_t ld_mbits, float *out,
            int64_t ldo, cudaStream_t st) {
     const size_t smem = (size_t)WARPS * S * NCH * 32 * 16;   // 32/G streams per warp
     static int blocks_per_sm = 0, n_sm = 0;
@@ -245,7 +253,7 @@ int launch_epi(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col,
     const int64_t blocks = ((n_rows + rpw - 1) / rpw + SPB - 1) / SPB;
     cgpdl::launch(k_spmm_cpa<G, NCH, S, EPI>, dim3((unsigned)blocks), dim3(WARPS * 32), smem, st,
                   n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, scale, addend, ld_add, mask,
-                  ld_mask, out, ldo, rpw, spmm_flags());
+                  ld_mask, mbits, ld_mbits, out, ldo, rpw, spmm_flags());
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 1 : cg_cuda_fail(e, "k_spmm_cpa");
 }
@@ -253,13 +261,16 @@ int launch_epi(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col,
 template <int G, int NCH, int S>
 int launch(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col, int64_t n_direct,
            const int32_t *halo_row, const float *X, int64_t ldx, const float *scale,
-           const float *addend, int64_t ld_add, const float *mask, int64_t ld_mask, float *out,
+           const float *addend, int64_t ld_add, const float *mask, int64_t ld_mask,
+           const uint32_t *mbits, int64_t ld_mbits, float *out,
            int64_t ldo, cudaStream_t st) {
-    return (addend || mask)
+    return (addend || mask || mbits)
                ? launch_epi<G, NCH, S, true>(n_rows, F, rowptr, col, n_direct, halo_row, X, ldx,
-                                          scale, addend, ld_add, mask, ld_mask, out, ldo, st)
+                                          scale, addend, ld_add, mask, ld_mask, mbits, ld_mbits, out, ldo,
+                                          st)
                : launch_epi<G, NCH, S, false>(n_rows, F, rowptr, col, n_direct, halo_row, X, ldx,
-                                           scale, addend, ld_add, mask, ld_mask, out, ldo, st);
+                                           scale, addend, ld_add, mask, ld_mask, mbits, ld_mbits, out, ldo,
+                                          st);
 }
 
 }  // namespace cpa
@@ -273,12 +284,14 @@ template <int G, int NCH, int... Ss>
 int launch_s(int S, int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col,
              int64_t n_direct, const int32_t *halo_row, const float *X, int64_t ldx,
              const float *scale, const float *addend, int64_t ld_add, const float *mask,
-             int64_t ld_mask, float *out, int64_t ldo, cudaStream_t st) {
+             int64_t ld_mask, const uint32_t *mbits, int64_t ld_mbits, float *out, int64_t ldo,
+             cudaStream_t st) {
     int rc = 0;
     bool hit = false;
     ((S == Ss && !hit
           ? (hit = true, rc = cpa::launch<G, NCH, Ss>(n_rows, F, rowptr, col, n_direct, halo_row, X,
-                                                   ldx, scale, addend, ld_add, mask, ld_mask, out,
+                                                   ldx, scale, addend, ld_add, mask, ld_mask,
+                                                   mbits, ld_mbits, out,
                                                    ldo, st))
           : 0),
      ...);
@@ -291,12 +304,13 @@ int launch_s(int S, int64_t n_rows, int F, const int64_t *rowptr, const int32_t 
 int cg_spmm_async(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col,
                   int64_t n_direct, const int32_t *halo_row, const float *X, int64_t ldx,
                   const float *scale, const float *addend, int64_t ld_add, const float *mask,
-                  int64_t ld_mask, float *out, int64_t ldo, cudaStream_t st) {
+                  int64_t ld_mask, const uint32_t *mbits, int64_t ld_mbits, float *out, int64_t ldo,
+             cudaStream_t st) {
     if (F > 640 || F % 4 || ldx % 4) return 0;
     static const int S = getenv("CG_SPMM_S") ? atoi(getenv("CG_SPMM_S")) : SPMM_CPA_S;
     static const bool narrow_g4 = !getenv("CG_SPMM_G4") || atoi(getenv("CG_SPMM_G4")) != 0;
 #define CG_CPA_ARGS n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, scale, addend, ld_add, \
-                    mask, ld_mask, out, ldo, st
+                    mask, ld_mask, mbits, ld_mbits, out, ldo, st
     // lanes per edge stream: CG_SPMM_LANES picks fewer lanes (more 16-byte
     // chunks per lane, fewer per-edge instructions per byte) for F <= 256
     static const int lanes = getenv("CG_SPMM_LANES") ? atoi(getenv("CG_SPMM_LANES")) : 0;
@@ -312,7 +326,7 @@ int cg_spmm_async(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *c
         // 0.088 -> 0.078 ms, 256-wide as two slices 0.197 -> 0.184 ms); the
         // epilogue variant (addend / mask prefetch registers scale with the
         // chunks per lane: 150 registers) stays on 16 lanes (0.21 vs 0.33 ms)
-        const bool epi = addend != nullptr || mask != nullptr;
+        const bool epi = addend != nullptr || mask != nullptr || mbits != nullptr;
         if (lanes == 16 || (lanes == 0 && epi)) return launch_s<16, 2, 4, 8>(S, CG_CPA_ARGS);
         if (lanes == 4) return launch_s<4, 8, 3, 4>(S, CG_CPA_ARGS);
         return launch_s<8, 4, 4, 6>(S, CG_CPA_ARGS);

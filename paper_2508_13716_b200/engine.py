@@ -231,7 +231,8 @@ class Engine:
         # epoch-1 snapshot copy -- the same values, half the distinct rows
         # the layer-0 gather touches (C2: 334K -> 169K rows, within L2)
         self.halo_row0 = None
-        if self.L.compact and D.n_halo and self.L.union is not None and self.L.union.size:
+        if (self.L.compact and D.n_halo and self.L.union is not None and self.L.union.size
+                and os.environ.get("CG_L0_OWNER", "1") != "0"):
             k = np.searchsorted(self.L.union, D.halo_vertex)
             own = self.L.owner_dev[k] == self.me
             h0 = np.where(own, self.L.owner_row[k], D.snap_row_of_pos).astype(np.int32)
@@ -266,6 +267,16 @@ class Engine:
         self._tabG_lds = {}
         # aggregated narrow gradients (backward aggregate-then-transform layers)
         self.T = torch.zeros(D.n_in, max(self.dims[1:]), dtype=f32, device=dev)
+        # ReLU masks as bits (layer l >= 1 inputs are ReLU outputs): written by
+        # the forward GEMM's epilogue, read by the masked backward GEMM / SpMM
+        # instead of the fp32 activation rows (1/32 of the bytes).  Needs the
+        # tcgen05 GEMM and 32-column tiles; CG_MASK_BITS=0 keeps fp32 masks.
+        self.bits = {}
+        if self.gemm_mode in (1, 2) and os.environ.get("CG_MASK_BITS", "1") != "0":
+            for l in range(1, self.nL):
+                Fl = self.F[l]
+                if Fl % 32 == 0 and (Fl <= 128 or Fl % 128 == 0):
+                    self.bits[l] = torch.zeros(D.n_in, Fl // 32, dtype=torch.int32, device=dev)
         # frozen-plan (K6) state, created at hand-off
         self.k6 = None
         self._io = None
@@ -300,7 +311,8 @@ class Engine:
              ptr(self.paramsT_hi), ptr(self.paramsT_lo), mx, self.stream())
 
     def _gemm(self, M, N, K1, A1, lda1, w1, K2=0, A2=None, lda2=0, w2=None, *, trans_b,
-              bias=None, relu=0, row_scale=None, mask=None, ldm=0, C, ldc):
+              bias=None, relu=0, row_scale=None, mask=None, ldm=0, C, ldc, mask_l=None,
+              bits_l=None):
         """cg_gemm with weight operands given as parameter indices: under
         3xTF32 the weights are read pre-split (params_hi / params_lo, kept
         current by cg_adam), so the kernel splits only the activations."""
@@ -316,15 +328,36 @@ class Engine:
             L1, L2 = b(w1, self.params_lo), b(w2, self.params_lo)
         else:
             B1, B2, L1, L2 = b(w1, self.params), b(w2, self.params), None, None
+        mb = self.bits.get(mask_l) if mask_l is not None else None
+        bo = self.bits.get(bits_l) if bits_l is not None else None
+        if mb is not None or bo is not None:
+            # ReLU masks as bits: layer mask_l's pattern in, layer bits_l's out
+            call("cg_gemm_mb", M, N, K1, A1, lda1, B1, K2, A2, lda2, B2, trans_b, bias, relu,
+                 row_scale, None if mb is None else ptr(mb),
+                 0 if mb is None else mb.shape[1], None if bo is None else ptr(bo),
+                 0 if bo is None else bo.shape[1], C, ldc, self.gemm_mode, L1, L2,
+                 self.stream())
+            return
+        if mask_l is not None:
+            mask, ldm = ptr(self.X[mask_l]), self.F[mask_l]
         call("cg_gemm", M, N, K1, A1, lda1, B1, K2, A2, lda2, B2, trans_b, bias, relu,
              row_scale, mask, ldm, C, ldc, self.gemm_mode, L1, L2, self.stream())
 
     def _spmm(self, n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, scale, addend, ld_add,
-              mask, ld_mask, out, ldo):
+              mask, ld_mask, out, ldo, mask_l=None):
         """One cg_spmm call over tensors (the kernel choice and any column
-        slicing happen behind the C ABI)."""
+        slicing happen behind the C ABI).  mask_l: the ReLU mask is layer
+        mask_l's input (its bits when kept, else the fp32 rows)."""
         p = lambda t: None if t is None else ptr(t)  # noqa: E731
         nnz = self.D.nnz_fwd if rowptr is self.fwd_rowptr else self.D.nnz_bwd
+        if mask_l is not None:
+            mb = self.bits.get(mask_l)
+            if mb is not None:
+                call("cg_spmm_mb", n_rows, F, ptr(rowptr), ptr(col), n_direct, p(halo_row),
+                     ptr(X), ldx, p(scale), p(addend), ld_add, ptr(mb), mb.shape[1], ptr(out),
+                     ldo, int(nnz), self.stream())
+                return
+            mask, ld_mask = self.X[mask_l], self.F[mask_l]
         call("cg_spmm", n_rows, F, ptr(rowptr), ptr(col), n_direct, p(halo_row), ptr(X), ldx,
              p(scale), p(addend), ld_add, p(mask), ld_mask, ptr(out), ldo, int(nnz),
              self.stream())
@@ -683,14 +716,16 @@ class Engine:
             out = self.logits if last else self.X[l + 1]
             if last and not self._capturing:
                 self._wait_logits_download()
+            bl = None if last else l + 1   # this ReLU output's bits (backward masks)
             if kind == "gcn":
                 self._gemm(n_in, Fo, F, ptr(self.Z[l]), F, 2 * l, trans_b=0,
                            bias=self._p(2 * l + 1), relu=0 if last else 1,
-                           row_scale=None if last else ptr(self.norm_src), C=ptr(out), ldc=Fo)
+                           row_scale=None if last else ptr(self.norm_src), C=ptr(out), ldc=Fo,
+                           bits_l=bl)
             else:
                 self._gemm(n_in, Fo, F, ptr(self.X[l]), F, 3 * l, F, ptr(self.Z[l]), F,
                            3 * l + 1, trans_b=0, bias=self._p(3 * l + 2),
-                           relu=0 if last else 1, C=ptr(out), ldc=Fo)
+                           relu=0 if last else 1, C=ptr(out), ldc=Fo, bits_l=bl)
 
     def _wait_logits_download(self) -> None:
         # the previous epoch's logits download must finish before they change
@@ -769,16 +804,16 @@ class Engine:
             else:
                 self._spmm(n_in, F, self.bwd_rowptr, self.bwd_col, 1 << 62, None, G, F,
                            self.norm_src if kind == "gcn" else None,
-                           self.Hs if kind == "sage" else None, F, self.X[l], F, nxt, F)
+                           self.Hs if kind == "sage" else None, F, None, 0, nxt, F, mask_l=l)
             if spmm_ev is not None:
                 self._rec(spmm_ev[k][1])
             if wide:
                 if kind == "gcn":
-                    self._gemm(n_in, F, Fo, ptr(self.T), Fo, W, trans_b=1, mask=ptr(self.X[l]),
-                               ldm=F, C=ptr(nxt), ldc=F)
+                    self._gemm(n_in, F, Fo, ptr(self.T), Fo, W, trans_b=1, mask_l=l,
+                               C=ptr(nxt), ldc=F)
                 else:
                     self._gemm(n_in, F, Fo, ptr(dY), Fo, 3 * l, Fo, ptr(self.T), Fo, W,
-                               trans_b=1, mask=ptr(self.X[l]), ldm=F, C=ptr(nxt), ldc=F)
+                               trans_b=1, mask_l=l, C=ptr(nxt), ldc=F)
             if l != nL - 1:
                 cur = 1 - cur
 

@@ -330,3 +330,75 @@ def test_split_tf32_transposed():
         ht = h[o:o + r * c].reshape(c, r)
         lt = lw[o:o + r * c].reshape(c, r)
         _check_tf32_split(m.T, ht, lt)
+
+
+def _pack_bits(x):
+    """(rows, F) -> (rows, F // 32) int32: bit j of word w = x[:, 32 w + j] > 0."""
+    b = (np.asarray(x) > 0).reshape(x.shape[0], -1, 32).astype(np.uint64)
+    w = (b << np.arange(32, dtype=np.uint64)).sum(-1).astype(np.uint32)
+    return w.view(np.int32)
+
+
+@pytest.mark.parametrize("shape", [(2000, 256, 128, 0), (777, 128, 64, 1), (1500, 64, 40, 1),
+                                   (900, 256, 256, 0)], ids=lambda s: "x".join(map(str, s)))
+def test_relu_bits_out_and_masked_gemm_bits(shape):
+    """cg_gemm_mb: a ReLU layer's bits_out equals the > 0 pattern of the
+    stored output exactly, and a mask-bits GEMM equals the fp32-mask GEMM
+    bit for bit (same kernel arithmetic, only the mask operand differs)."""
+    import torch
+    from paper_2508_13716_b200._lib import call, ptr
+    M, N, K, tb = shape
+    rng = np.random.default_rng(M + N + K)
+    A = _t(rng.standard_normal((M, K)).astype(np.float32))
+    B = _t(rng.standard_normal((N, K) if tb else (K, N)).astype(np.float32))
+    Bh, Bl = torch.empty_like(B), torch.empty_like(B)
+    call("cg_split_tf32", B.numel(), ptr(B), ptr(Bh), ptr(Bl), _st())
+    bias = _t(rng.standard_normal(N).astype(np.float32))
+    rs = _t(rng.random(M).astype(np.float32))
+    out = torch.empty(M, N, device="cuda")
+    bits = torch.full((M, N // 32), -1, dtype=torch.int32, device="cuda")
+    call("cg_gemm_mb", M, N, K, ptr(A), K, ptr(Bh), 0, None, 0, None, tb, ptr(bias), 1, ptr(rs),
+         None, 0, ptr(bits), N // 32, ptr(out), N, 1, ptr(Bl), None, _st())
+    _sync()
+    assert np.array_equal(bits.cpu().numpy(), _pack_bits(out.cpu().numpy()))
+    # masked GEMM: fp32 mask = out, vs its bits
+    ref = torch.empty(M, N, device="cuda")
+    got = torch.empty(M, N, device="cuda")
+    call("cg_gemm", M, N, K, ptr(A), K, ptr(Bh), 0, None, 0, None, tb, None, 0, None, ptr(out),
+         N, ptr(ref), N, 1, ptr(Bl), None, _st())
+    call("cg_gemm_mb", M, N, K, ptr(A), K, ptr(Bh), 0, None, 0, None, tb, None, 0, None,
+         ptr(bits), N // 32, None, 0, ptr(got), N, 1, ptr(Bl), None, _st())
+    _sync()
+    assert torch.equal(ref, got)
+    assert (ref == 0).any() and (ref != 0).any()
+
+
+@pytest.mark.parametrize("F", [32, 128, 256])
+@pytest.mark.parametrize("sparse", [False, True])
+def test_spmm_mask_bits_equal_fp32_mask(F, sparse):
+    """cg_spmm_mb (mask as bits) == cg_spmm (fp32 mask) bit for bit, on both
+    SpMM kernels and across the 128-column slices."""
+    import torch
+    from paper_2508_13716_b200._lib import call, ptr
+    rng = np.random.default_rng(F)
+    n_rows, n_src = 3000, 5000
+    deg = rng.integers(0, 16, n_rows)
+    rowptr = np.concatenate(([0], np.cumsum(deg))).astype(np.int64)
+    col = np.sort(rng.integers(0, n_src, rowptr[-1]).astype(np.int32))
+    X = _t(rng.standard_normal((n_src, F)).astype(np.float32))
+    mask = rng.standard_normal((n_rows, F)).astype(np.float32)
+    tm, tb_ = _t(mask), _t(_pack_bits(mask))
+    add = _t(rng.standard_normal((n_rows, F)).astype(np.float32))
+    sc = _t(rng.random(n_rows).astype(np.float32))
+    tr, tc = _t(rowptr), _t(col)
+    nnz = int(rowptr[-1]) if sparse else -1
+    for addend in (None, add):
+        a = torch.empty(n_rows, F, device="cuda")
+        b = torch.empty(n_rows, F, device="cuda")
+        ap = None if addend is None else ptr(addend)
+        call("cg_spmm", n_rows, F, ptr(tr), ptr(tc), 1 << 62, None, ptr(X), F, ptr(sc), ap, F,
+             ptr(tm), F, ptr(a), F, nnz, _st())
+        call("cg_spmm_mb", n_rows, F, ptr(tr), ptr(tc), 1 << 62, None, ptr(X), F, ptr(sc), ap, F,
+             ptr(tb_), F // 32, ptr(b), F, nnz, _st())
+        _sync()
+        assert torch.equal(a, b)
