@@ -220,10 +220,11 @@ def run_ours(args):
     # ---- SpMM roofline (all fwd+bwd aggregation launches of the timed epochs)
     fwd_ms = np.array([s.spmm_fwd_ms for s in stats])  # (K, L)
     bwd_ms = np.array([s.spmm_bwd_ms for s in stats])  # (K, L-1)
-    fb = [spmm_bytes(D.nnz_fwd, D.n_in, F, D.n_halo) for F in F_DIM]
-    widths = list(F_DIM) + [eng.C4]   # backward aggregates min(F_in, F_out) wide
-    bb = [spmm_bytes(D.nnz_bwd, D.n_in, min(widths[l], widths[l + 1]), 0)
-          for l in range(len(F_DIM) - 1, 0, -1)]
+    # aggregation widths in launch order (backward: min(F_in, F_out) wide;
+    # GraphSAGE layer 0 transform-first when it narrows adds a backward one)
+    fw, bw = eng.spmm_widths()
+    fb = [spmm_bytes(D.nnz_fwd, D.n_in, F, D.n_halo) for F in fw]
+    bb = [spmm_bytes(D.nnz_bwd, D.n_in, F, 0) for F in bw]
     tot_bytes = args.steps * (sum(fb) + sum(bb))
     tot_ms = float(fwd_ms.sum() + bwd_ms.sum())
     achieved = tot_bytes / (tot_ms / 1e3) / 1e9
@@ -346,9 +347,7 @@ def run_ours(args):
                                        "ms": round(float(m), 4),
                                        "GB_s": round(b_ / (float(m) / 1e3) / 1e9, 1)}
                                       for ps_, w, b_, m in zip(
-                                          ["fwd"] * len(fb) + ["bwd"] * len(bb),
-                                          list(F_DIM) + [min(widths[l], widths[l + 1])
-                                                         for l in range(len(F_DIM) - 1, 0, -1)],
+                                          ["fwd"] * len(fb) + ["bwd"] * len(bb), fw + bw,
                                           fb + bb,
                                           list(fwd_ms.mean(0)) + list(bwd_ms.mean(0)))]},
             "halo_bytes_per_epoch": {"model_fwd_cached": fwd_model,
@@ -378,23 +377,32 @@ def sum_over_ranks(x, world: int, backend: str):
 
 
 def l2_peak(nbytes: int = 24 << 20, reps: int = 50) -> float:
-    """L2 bandwidth, GB/s: a device copy between two L2-resident buffers
-    (2 x 24 MB << 126 MB), read + write bytes, best of 5 batches."""
+    """L2 bandwidth, GB/s, measured: the better of a device copy between two
+    L2-resident buffers (2 x 24 MB << 126 MB; read + write bytes) and a
+    read-only column reduction of a 48 MB L2-resident buffer (the SpMM's
+    gathers are reads), best of 5 batches each."""
     import torch
     a = torch.empty(nbytes // 4, dtype=torch.float32, device="cuda").uniform_()
     b = torch.empty_like(a)
-    for _ in range(3):
-        b.copy_(a)
-    best = 1e9
-    for _ in range(5):
-        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0.record()
-        for _ in range(reps):
-            b.copy_(a)
-        t1.record()
-        torch.cuda.synchronize()
-        best = min(best, t0.elapsed_time(t1) / reps)
-    return 2 * nbytes / (best / 1e3) / 1e9
+    r = torch.empty(2 * nbytes // 4 // 1024, 1024, dtype=torch.float32, device="cuda").uniform_()
+    o = torch.empty(1024, dtype=torch.float32, device="cuda")
+
+    def best_ms(fn):
+        for _ in range(3):
+            fn()
+        best = 1e9
+        for _ in range(5):
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0.record()
+            for _ in range(reps):
+                fn()
+            t1.record()
+            torch.cuda.synchronize()
+            best = min(best, t0.elapsed_time(t1) / reps)
+        return best
+    copy = 2 * nbytes / (best_ms(lambda: b.copy_(a)) / 1e3) / 1e9
+    read = 2 * nbytes / (best_ms(lambda: torch.sum(r, dim=0, out=o)) / 1e3) / 1e9
+    return max(copy, read)
 
 
 def pcie_peaks(nbytes: int = 256 << 20):

@@ -167,6 +167,14 @@ int cg_split_tf32(int64_t n, const float *x, float *hi, float *lo, void *stream)
  * K-major (one TMA box per k-block) weight operand.                      */
 int cg_split_tf32_t(int n_mats, const int64_t *off, const int32_t *rows, const int32_t *cols,
                     const float *x, float *hi, float *lo, int64_t max_elems, void *stream);
+/* The bf16 cross-term operand of gemm mode 3 for n_mats K-major weights:
+ * matrix m is hi / lo [n_rows[m] x k_cols[m]] row-major at in_off[m]; out
+ * at out_off[m] is [n_rows x 2 Kp] bf16 (Kp = k_cols rounded up to 32), per
+ * 32-wide k-block the bf16 of the block's hi values then of its lo values,
+ * zero past K.  max_elems = max over m of n_rows * 2 Kp.                  */
+int cg_pack_bx(int n_mats, const int64_t *in_off, const int32_t *n_rows, const int32_t *k_cols,
+               const float *hi, const float *lo, uint16_t *out, const int64_t *out_off,
+               int64_t max_elems, void *stream);
 /* dW[k, n] = sum_m A[m, k] * D[m, n]; deterministic split over m.
  * db (optional): db[n] = sum_m D[m, n] (the bias gradient) -- under 3xTF32
  * fused into the same kernel (column sums while D is staged in smem).
@@ -177,6 +185,12 @@ int cg_wgrad(int64_t M, int K, int N, const float *A, int64_t lda, const float *
 /* db[n] = sum_m D[m, n] (deterministic); ws as for cg_wgrad with K = 1.  */
 int cg_colsum(int64_t M, int N, const float *D, int64_t ldd, float *db, float *ws,
               void *stream);
+/* X = max(X, 0) in place (n_rows x F, F % 32 == 0) and, when bits is not
+ * NULL, the result's > 0 pattern as bits (format as cg_spmm_mb's mask):
+ * the ReLU of a layer whose pre-activation an aggregation produced (the
+ * GraphSAGE layer-0 transform-first order).                 */
+int cg_relu_bits(int64_t n_rows, int F, float *X, int64_t ldx, uint32_t *bits, int64_t ld_bits,
+                 void *stream);
 
 /* ---- K8: softmax cross-entropy ---------------------------------------- */
 /* grad[r, c] = (softmax(logits[r]) - onehot(label[r])) * inv_n;

@@ -56,12 +56,14 @@ SIGNATURES = {
     "cg_flag_wait": [P, INT, INT, C.c_uint32, P],
     "cg_spmm": [I64, INT, P, P, I64, P, P, I64, P, P, I64, P, I64, P, I64, I64, P],
     "cg_spmm_mb": [I64, INT, P, P, I64, P, P, I64, P, P, I64, P, I64, P, I64, I64, P],
+    "cg_relu_bits": [I64, INT, P, I64, P, I64, P],
     "cg_gemm_mb": [I64, INT, INT, P, I64, P, INT, P, I64, P, INT, P, INT, P, P, I64, P, I64, P,
                    I64, INT, P, P, P],
     "cg_gemm": [I64, INT, INT, P, I64, P, INT, P, I64, P, INT, P, INT, P, P, I64, P, I64, INT,
                 P, P, P],
     "cg_split_tf32": [I64, P, P, P, P],
     "cg_split_tf32_t": [INT, P, P, P, P, P, P, I64, P],
+    "cg_pack_bx": [INT, P, P, P, P, P, P, P, I64, P],
     "cg_wgrad_workspace": [I64, INT, INT],
     "cg_wgrad": [I64, INT, INT, P, I64, P, I64, P, P, P, INT, P],
     "cg_colsum": [I64, INT, P, I64, P, P, P],
@@ -125,8 +127,9 @@ def lib():
 # total is the bench's "gpu_launches" evidence
 KERNEL_ENTRY = {"cg_hash_features", "cg_hash_labels", "cg_scale_rows", "cg_scale_rows_to",
                 "cg_copy_rows", "cg_copy_rows_bounded", "cg_copy_rows_sel",
-                "cg_spmm", "cg_spmm_mb", "cg_gemm", "cg_gemm_mb", "cg_wgrad", "cg_colsum", "cg_softmax_ce", "cg_adam",
-                "cg_split_tf32", "cg_split_tf32_t",
+                "cg_spmm", "cg_spmm_mb", "cg_relu_bits", "cg_gemm", "cg_gemm_mb", "cg_wgrad",
+                "cg_colsum", "cg_softmax_ce", "cg_adam",
+                "cg_split_tf32", "cg_split_tf32_t", "cg_pack_bx",
                 "cg_plan_frozen", "cg_set_epoch"}
 launches = {"total": 0}
 

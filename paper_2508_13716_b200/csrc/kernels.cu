@@ -10,6 +10,7 @@
 // All reductions are fixed-order (no float atomics): reruns are bitwise
 // identical.  See DESIGN.md for layouts and rooflines.
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -611,6 +612,31 @@ __global__ void k_scale_rows(float *__restrict__ X, int64_t ld, int64_t n, int F
     }
 }
 
+// X = max(X, 0) in place over rows of F columns (F % 32 == 0), and the
+// > 0 pattern as bits: one thread per 32-column word (eight float4s).
+__global__ void k_relu_bits(int64_t n_rows, int F, float *__restrict__ X, int64_t ldx,
+                            uint32_t *__restrict__ bits, int64_t ld_bits) {
+    pdl_entry();
+    const int W = F >> 5;
+    const int64_t n = n_rows * W;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / W;
+        const int w = (int)(i - r * W);
+        float4 *p = reinterpret_cast<float4 *>(X + r * ldx) + 8 * w;
+        uint32_t b = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            float4 v = p[j];
+            v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
+            b |= ((v.x > 0.f ? 1u : 0u) | (v.y > 0.f ? 2u : 0u) | (v.z > 0.f ? 4u : 0u) |
+                  (v.w > 0.f ? 8u : 0u)) << (4 * j);
+            p[j] = v;
+        }
+        if (bits) bits[r * ld_bits + w] = b;
+    }
+}
+
 __global__ void k_scale_rows_to(float *__restrict__ dst, int64_t ldd, const float *__restrict__ src,
                                 int64_t lds, int64_t n, int F, const float *__restrict__ scale) {
     int64_t total = n * (int64_t)F;
@@ -692,6 +718,30 @@ __global__ void k_split_tf32_t(const int64_t *__restrict__ off, const int32_t *_
     split_tf32(x[o + e], h, l);
     hi[o + (int64_t)j * r + i] = h;
     lo[o + (int64_t)j * r + i] = l;
+}
+
+// The 3xTF32 GEMM's bf16 cross-term operand (mode 3): for a K-major weight
+// split into (hi, lo) [N x K], out [N x 2 Kp] bf16 (Kp = K rounded up to 32)
+// holds per 32-wide k-block kb the 64 values
+//   bf16(hi[n, 32 kb .. 32 kb + 31]) | bf16(lo[n, 32 kb .. 32 kb + 31])
+// (zero past K) -- one 128-byte TMA row per k-block, matching the A' operand
+// [A_lo | A] the GEMM's splitter packs.
+__global__ void k_pack_bx(const int64_t *__restrict__ in_off, const int32_t *__restrict__ nrows,
+                          const int32_t *__restrict__ kcols, const float *__restrict__ hi,
+                          const float *__restrict__ lo, uint16_t *__restrict__ out,
+                          const int64_t *__restrict__ out_off) {
+    pdl_entry();
+    const int m = blockIdx.y;
+    const int N = nrows[m], K = kcols[m];
+    const int Kp2 = 2 * ((K + 31) / 32 * 32);
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= (int64_t)N * Kp2) return;
+    const int n = (int)(e / Kp2), q = (int)(e % Kp2);
+    const int kb = q >> 6, j = q & 63;
+    const int k = 32 * kb + (j & 31);
+    float v = 0.f;
+    if (k < K) v = (j < 32 ? hi : lo)[in_off[m] + (int64_t)n * K + k];
+    out[out_off[m] + e] = __bfloat16_as_ushort(__float2bfloat16_rn(v));
 }
 
 __global__ void k_split_tf32(int64_t n, const float *__restrict__ x, float *__restrict__ hi,
@@ -1099,6 +1149,19 @@ int cg_scale_rows_to(float *dst, int64_t ldd, const float *src, int64_t lds, int
     return 1;
 }
 
+int cg_relu_bits(int64_t n_rows, int F, float *X, int64_t ldx, uint32_t *bits, int64_t ld_bits,
+                 void *stream) {
+    if (n_rows == 0 || F == 0) return 0;
+    if (F % 32 || ldx % 4 || ((uintptr_t)X % 16)) {
+        cg_set_error("cg_relu_bits: F % 32 == 0, ldx % 4 == 0 and a 16-byte aligned X needed");
+        return -1;
+    }
+    cgpdl::launch(k_relu_bits, dim3(grid_for(n_rows * (F / 32), 256, n_sms() * 8)), dim3(256), 0,
+                  (cudaStream_t)stream, n_rows, F, X, ldx, bits, ld_bits);
+    CG_CHECK_LAUNCH("k_relu_bits");
+    return 1;
+}
+
 int cg_colsum(int64_t M, int N, const float *D, int64_t ldd, float *db, float *ws, void *stream) {
     if (M == 0 || N == 0) return 0;
     int64_t nch = (M + kColChunk - 1) / kColChunk;
@@ -1207,6 +1270,17 @@ int cg_split_tf32_t(int n_mats, const int64_t *off, const int32_t *rows, const i
     cgpdl::launch(k_split_tf32_t, grid, dim3(256), 0, (cudaStream_t)stream, off, rows, cols, x,
                   hi, lo);
     CG_CHECK_LAUNCH("k_split_tf32_t");
+    return 1;
+}
+
+int cg_pack_bx(int n_mats, const int64_t *in_off, const int32_t *n_rows, const int32_t *k_cols,
+               const float *hi, const float *lo, uint16_t *out, const int64_t *out_off,
+               int64_t max_elems, void *stream) {
+    if (n_mats == 0 || max_elems == 0) return 0;
+    dim3 grid((unsigned)((max_elems + 255) / 256), (unsigned)n_mats);
+    cgpdl::launch(k_pack_bx, grid, dim3(256), 0, (cudaStream_t)stream, in_off, n_rows, k_cols, hi,
+                  lo, out, out_off);
+    CG_CHECK_LAUNCH("k_pack_bx");
     return 1;
 }
 

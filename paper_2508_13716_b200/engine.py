@@ -179,11 +179,37 @@ class Engine:
                             _dev([self.pshapes[i][0] for i in mats], torch.int32, dev),
                             _dev([self.pshapes[i][1] for i in mats], torch.int32, dev),
                             len(mats), max(int(np.prod(self.pshapes[i])) for i in mats))
+            # mode 3 (CG_GEMM_BX=1): the forward / input-gradient GEMMs take
+            # their cross terms as one bf16 MMA against packed weights
+            self.use_bx = os.environ.get("CG_GEMM_BX", "0") == "1"
+            if self.use_bx:
+                def kp2(k):
+                    return 2 * ((k + 31) // 32 * 32)
+                offT, off, totT, tot = {}, {}, 0, 0
+                for i in mats:
+                    fi, fo = self.pshapes[i]
+                    offT[i], off[i] = totT, tot
+                    totT += fo * kp2(fi)
+                    tot += fi * kp2(fo)
+                self._bx_offT, self._bx_off = offT, off
+                self.params_bxT = torch.zeros(max(totT, 8), dtype=torch.int16, device=dev)
+                self.params_bx = torch.zeros(max(tot, 8), dtype=torch.int16, device=dev)
+                i64 = torch.int64
+                self._bx_tabs = []
+                for T in (True, False):
+                    rows = [self.pshapes[i][1] if T else self.pshapes[i][0] for i in mats]
+                    cols = [self.pshapes[i][0] if T else self.pshapes[i][1] for i in mats]
+                    outo = [(offT if T else off)[i] for i in mats]
+                    self._bx_tabs.append((
+                        _dev([int(self.poff[i]) for i in mats], i64, dev), _dev(rows, torch.int32, dev),
+                        _dev(cols, torch.int32, dev), _dev(outo, i64, dev), len(mats),
+                        max(r * kp2(c) for r, c in zip(rows, cols)), T))
             call("cg_split_tf32", self.n_params, ptr(self.params), ptr(self.params_hi),
                  ptr(self.params_lo), self.stream())
             self._split_t()
         else:
             self.params_hi = self.params_lo = None
+            self.use_bx = False
         self.grads = torch.zeros(self.n_params + 1, dtype=f32, device=dev)
         self.adam_m = torch.zeros(self.n_params, dtype=f32, device=dev)
         self.adam_v = torch.zeros(self.n_params, dtype=f32, device=dev)
@@ -231,12 +257,29 @@ class Engine:
         # epoch-1 snapshot copy -- the same values, half the distinct rows
         # the layer-0 gather touches (C2: 334K -> 169K rows, within L2)
         self.halo_row0 = None
+        self.tf0 = False
         if (self.L.compact and D.n_halo and self.L.union is not None and self.L.union.size
                 and os.environ.get("CG_L0_OWNER", "1") != "0"):
             k = np.searchsorted(self.L.union, D.halo_vertex)
             own = self.L.owner_dev[k] == self.me
             h0 = np.where(own, self.L.owner_row[k], D.snap_row_of_pos).astype(np.int32)
             self.halo_row0 = _dev(h0, i32, dev)
+        # GraphSAGE layer 0, transform first when it narrows (F0 > F1, C3:
+        # 604 -> 256): Y = relu(X W_self + b + mean_N(X W_neigh)) aggregates
+        # F1-wide rows instead of F0-wide ones.  Exact when every layer-0
+        # source row is an inner row of this device (one process, the
+        # compact layout's owner-row halo map): the transformed rows are then
+        # this device's own.  The weight gradient needs the transposed
+        # aggregation of (1/d_in) dY over the out-edges (K2), instead of the
+        # saved F0-wide aggregate.  CG_SAGE_TF0=0 keeps aggregate-first.
+        self.tf0 = (self.kind == "sage" and self.nL >= 2 and self.F[0] > self.dims[1]
+                    and self.halo_row0 is not None and self.comm.world == 1
+                    and (not D.n_halo or bool((h0 < D.n_in).all()))
+                    and os.environ.get("CG_SAGE_TF0", "1") != "0")
+        if self.tf0:
+            F1 = self.dims[1]
+            self.tf0_h = torch.zeros(D.n_in, F1, dtype=f32, device=dev)   # X W_neigh
+            self.tf0_p = torch.zeros(D.n_in, F1, dtype=f32, device=dev)   # X W_self + b
         # backward staging lists
         nb = max(n_bwd, 1)
         self.b_src = _dev(D.bwd_src_dev if n_bwd else [-1], i32, dev)
@@ -309,6 +352,13 @@ class Engine:
         off, rows, cols, n, mx = self._wt_tab
         call("cg_split_tf32_t", n, ptr(off), ptr(rows), ptr(cols), ptr(self.params),
              ptr(self.paramsT_hi), ptr(self.paramsT_lo), mx, self.stream())
+        if getattr(self, "use_bx", False):
+            for in_off, rows, cols, out_off, n, mx, T in self._bx_tabs:
+                hi, lo = ((self.paramsT_hi, self.paramsT_lo) if T
+                          else (self.params_hi, self.params_lo))
+                call("cg_pack_bx", n, ptr(in_off), ptr(rows), ptr(cols), ptr(hi), ptr(lo),
+                     ptr(self.params_bxT if T else self.params_bx), ptr(out_off), mx,
+                     self.stream())
 
     def _gemm(self, M, N, K1, A1, lda1, w1, K2=0, A2=None, lda2=0, w2=None, *, trans_b,
               bias=None, relu=0, row_scale=None, mask=None, ldm=0, C, ldc, mask_l=None,
@@ -317,15 +367,25 @@ class Engine:
         3xTF32 the weights are read pre-split (params_hi / params_lo, kept
         current by cg_adam), so the kernel splits only the activations."""
         split = self.params_hi is not None
+        mode = self.gemm_mode
         def b(i, arr):
             return None if i is None else ptr(arr) + 4 * int(self.poff[i])
+        def bx(i, T):
+            if i is None:
+                return None
+            return ptr(self.params_bxT if T else self.params_bx) + 2 * (self._bx_offT if T
+                                                                         else self._bx_off)[i]
         if split and trans_b == 0:   # W [K x N] -> its transpose, K-major
             B1, B2 = b(w1, self.paramsT_hi), b(w2, self.paramsT_hi)
             L1, L2 = b(w1, self.paramsT_lo), b(w2, self.paramsT_lo)
+            if self.use_bx:
+                L1, L2, mode = bx(w1, True), bx(w2, True), 3
             trans_b = 1
         elif split:
             B1, B2 = b(w1, self.params_hi), b(w2, self.params_hi)
             L1, L2 = b(w1, self.params_lo), b(w2, self.params_lo)
+            if self.use_bx:
+                L1, L2, mode = bx(w1, False), bx(w2, False), 3
         else:
             B1, B2, L1, L2 = b(w1, self.params), b(w2, self.params), None, None
         mb = self.bits.get(mask_l) if mask_l is not None else None
@@ -335,13 +395,12 @@ class Engine:
             call("cg_gemm_mb", M, N, K1, A1, lda1, B1, K2, A2, lda2, B2, trans_b, bias, relu,
                  row_scale, None if mb is None else ptr(mb),
                  0 if mb is None else mb.shape[1], None if bo is None else ptr(bo),
-                 0 if bo is None else bo.shape[1], C, ldc, self.gemm_mode, L1, L2,
-                 self.stream())
+                 0 if bo is None else bo.shape[1], C, ldc, mode, L1, L2, self.stream())
             return
         if mask_l is not None:
             mask, ldm = ptr(self.X[mask_l]), self.F[mask_l]
         call("cg_gemm", M, N, K1, A1, lda1, B1, K2, A2, lda2, B2, trans_b, bias, relu,
-             row_scale, mask, ldm, C, ldc, self.gemm_mode, L1, L2, self.stream())
+             row_scale, mask, ldm, C, ldc, mode, L1, L2, self.stream())
 
     def _spmm(self, n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, scale, addend, ld_add,
               mask, ld_mask, out, ldo, mask_l=None):
@@ -701,6 +760,9 @@ class Engine:
                 # have been staged (a host-plan epoch may reassign a slot read
                 # above): write the dirty global entries through
                 self._gw(l)
+            if l == 0 and self.tf0:
+                self._forward_tf0(spmm_ev)
+                continue
             if spmm_ev is not None:
                 self._rec(spmm_ev[l][0])
             hrow = self.halo_row0 if (l == 0 and self.halo_row0 is not None) else self.halo_row
@@ -726,6 +788,37 @@ class Engine:
                 self._gemm(n_in, Fo, F, ptr(self.X[l]), F, 3 * l, F, ptr(self.Z[l]), F,
                            3 * l + 1, trans_b=0, bias=self._p(3 * l + 2),
                            relu=0 if last else 1, C=ptr(out), ldc=Fo, bits_l=bl)
+
+    def _forward_tf0(self, spmm_ev) -> None:
+        """GraphSAGE layer 0, transform first (see _alloc): two GEMMs, one
+        F1-wide aggregation with the self term as its addend, then ReLU (and
+        the backward mask bits) in place."""
+        n_in, F, Fo = self.D.n_in, self.F[0], self.dims[1]
+        self._gemm(n_in, Fo, F, ptr(self.X[0]), F, 0, trans_b=0, bias=self._p(2), C=ptr(self.tf0_p),
+                   ldc=Fo)
+        self._gemm(n_in, Fo, F, ptr(self.X[0]), F, 1, trans_b=0, C=ptr(self.tf0_h), ldc=Fo)
+        if spmm_ev is not None:
+            self._rec(spmm_ev[0][0])
+        self._spmm(n_in, Fo, self.fwd_rowptr, self.fwd_col, n_in, self.halo_row0, self.tf0_h, Fo,
+                   self.norm_dst, self.tf0_p, Fo, None, 0, self.X[1], Fo)
+        if spmm_ev is not None:
+            self._rec(spmm_ev[0][1])
+        b = self.bits.get(1)
+        call("cg_relu_bits", n_in, Fo, ptr(self.X[1]), Fo, None if b is None else ptr(b),
+             0 if b is None else b.shape[1], self.stream())
+
+    def _n_bwd_spmm(self) -> int:
+        return self.nL - 1 + (1 if self.tf0 else 0)
+
+    def spmm_widths(self):
+        """Row widths of the epoch's aggregations in launch order: (forward
+        per layer, backward layers nL-1 .. 1 [, layer 0 under tf0])."""
+        w = list(self.F) + [self.C4]
+        fwd = [self.dims[1] if (l == 0 and self.tf0) else self.F[l] for l in range(self.nL)]
+        bwd = [min(w[l], w[l + 1]) for l in range(self.nL - 1, 0, -1)]
+        if self.tf0:
+            bwd.append(self.dims[1])
+        return fwd, bwd
 
     def _wait_logits_download(self) -> None:
         # the previous epoch's logits download must finish before they change
@@ -763,6 +856,23 @@ class Engine:
             if kind == "gcn":
                 call("cg_wgrad", n_in, F, Fo, ptr(self.Z[l]), F, ptr(dY), Fo, self._g(2 * l),
                      self._g(2 * l + 1), ptr(self.ws), self.wgrad_mode, st)
+            elif l == 0 and self.tf0:
+                # dW_self (+ db) as usual; dW_neigh = X^T T with T = A^T ((1/d_in) dY),
+                # the transposed aggregation over the out-edges (every source of
+                # the layer-0 aggregation is an inner row of this device)
+                call("cg_wgrad", n_in, F, Fo, ptr(self.X[0]), F, ptr(dY), Fo, self._g(0),
+                     self._g(2), ptr(self.ws), self.wgrad_mode, st)
+                G = self.Gs[0]
+                call("cg_scale_rows_to", ptr(G), Fo, ptr(dY), Fo, n_in, Fo, ptr(self.norm_dst), st)
+                k = nL - 1
+                if spmm_ev is not None:
+                    self._rec(spmm_ev[k][0])
+                self._spmm(n_in, Fo, self.bwd_rowptr, self.bwd_col, 1 << 62, None, G, Fo, None,
+                           None, 0, None, 0, self.T, Fo)
+                if spmm_ev is not None:
+                    self._rec(spmm_ev[k][1])
+                call("cg_wgrad", n_in, F, Fo, ptr(self.X[0]), F, ptr(self.T), Fo, self._g(1),
+                     None, ptr(self.ws), self.wgrad_mode, st)
             else:
                 call("cg_wgrad", n_in, F, Fo, ptr(self.X[l]), F, ptr(dY), Fo, self._g(3 * l),
                      None, ptr(self.ws), self.wgrad_mode, st)
@@ -860,7 +970,7 @@ class Engine:
         later epoch.  SpMM timing events are external event nodes."""
         if not self.gpu_plan_ready:
             self._init_gpu_plan()
-        fwd_ev, bwd_ev = self._new_timers(self.nL), self._new_timers(self.nL - 1)
+        fwd_ev, bwd_ev = self._new_timers(self.nL), self._new_timers(self._n_bwd_spmm())
         for a, b in fwd_ev + bwd_ev:   # materialise the events before capture
             a.record()
             b.record()
@@ -944,7 +1054,7 @@ class Engine:
             t0 = torch.cuda.Event(enable_timing=True)
             t0.record()
         fwd_ev = self._new_timers(self.nL) if timers else None
-        bwd_ev = self._new_timers(self.nL - 1) if timers else None
+        bwd_ev = self._new_timers(self._n_bwd_spmm()) if timers else None
         self._k3_used = [] if (timers and self._k3_on) else None
         self._mark("plan")
         mode, hcounts, _ = self.plan(e)

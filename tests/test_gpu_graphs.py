@@ -19,6 +19,7 @@ CASES = [
     ("gcn", 500, 6.0, 4, (16, 32, 32), 7, "auto", "jaca", -1, 6, "3xtf32"),
     ("gcn", 500, 5.0, 3, (16, 32, 32), 6, 60, "jaca", 1, 7, "3xtf32"),
     ("sage", 500, 5.0, 3, (16, 32), 6, 60, "jaca", 2, 7, "fp32"),
+    ("sage", 500, 6.0, 4, (64, 32, 32), 7, "auto", "jaca", -1, 5, "3xtf32"),   # layer-0 tf0
 ]
 
 

@@ -64,6 +64,10 @@ CASES = [
     # (request coalescing: one staged row per vertex and device)
     ("gcn", 500, 5.0, 4, (16, 32, 32), 6, (20, 200), "jaca", 1, 5, "3xtf32"),
     ("sage", 600, 6.0, 4, (16, 32, 32), 6, (40, 300), "jaca", 2, 6, "3xtf32"),
+    # GraphSAGE layer 0 transform-first (F0 > F1, compact layout on one
+    # device): X W_neigh aggregated, the transposed aggregation in backward
+    ("sage", 500, 6.0, 4, (64, 32, 32), 7, "auto", "jaca", -1, 4, "3xtf32"),
+    ("sage", 500, 6.0, 4, (64, 32), 9, "auto", "jaca", -1, 3, "fp32"),
     # the SIMT fp32 GEMM (explicit opt-in)
     ("gcn", 500, 5.0, 3, (16, 32, 32), 6, 60, "jaca", 1, 4, "fp32"),
     ("sage", 400, 6.0, 4, (16, 32, 32), 7, "auto", "jaca", -1, 3, "fp32"),
@@ -274,3 +278,22 @@ def test_write_through_queue_matches_inline(monkeypatch):
     assert a.losses == b.losses
     for x, y in zip(a.logits_per_epoch, b.logits_per_epoch):
         assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("gemm", ["3xtf32", "fp32"])
+def test_sage_transform_first_layer0_matches_aggregate_first(gemm, monkeypatch):
+    """The two layer-0 orders of GraphSAGE (CG_SAGE_TF0) agree within the
+    parity bound every epoch, and the integer plan is identical."""
+    from paper_2508_13716_b200 import hostgraph as H
+    g, ps, og, ops = workload(600, 7.0, 4)
+    f_dim, C = (96, 32, 32), 6
+    caps = make_caps(H, ps, "auto", f_dim)
+    cfg = H.SimConfig(epochs=4, policy="jaca", staleness_bound=-1, f_dim=f_dim, L=3)
+    monkeypatch.setenv("CG_SAGE_TF0", "0")
+    a = _train(g, ps, caps, cfg, "sage", C, gemm=gemm, record_trace=True)
+    monkeypatch.setenv("CG_SAGE_TF0", "1")
+    b = _train(g, ps, caps, cfg, "sage", C, gemm=gemm, record_trace=True)
+    assert a.trace_csv == b.trace_csv
+    for e in range(4):
+        assert rel_err(b.logits_per_epoch[e], a.logits_per_epoch[e]) <= FREE_TOL[("sage", gemm)], e
+        assert abs(a.losses[e] - b.losses[e]) <= 1e-4 * abs(a.losses[e])
