@@ -167,14 +167,6 @@ int cg_split_tf32(int64_t n, const float *x, float *hi, float *lo, void *stream)
  * K-major (one TMA box per k-block) weight operand.                      */
 int cg_split_tf32_t(int n_mats, const int64_t *off, const int32_t *rows, const int32_t *cols,
                     const float *x, float *hi, float *lo, int64_t max_elems, void *stream);
-/* The bf16 cross-term operand of gemm mode 3 for n_mats K-major weights:
- * matrix m is hi / lo [n_rows[m] x k_cols[m]] row-major at in_off[m]; out
- * at out_off[m] is [n_rows x 2 Kp] bf16 (Kp = k_cols rounded up to 32), per
- * 32-wide k-block the bf16 of the block's hi values then of its lo values,
- * zero past K.  max_elems = max over m of n_rows * 2 Kp.                  */
-int cg_pack_bx(int n_mats, const int64_t *in_off, const int32_t *n_rows, const int32_t *k_cols,
-               const float *hi, const float *lo, uint16_t *out, const int64_t *out_off,
-               int64_t max_elems, void *stream);
 /* dW[k, n] = sum_m A[m, k] * D[m, n]; deterministic split over m.
  * db (optional): db[n] = sum_m D[m, n] (the bias gradient) -- under 3xTF32
  * fused into the same kernel (column sums while D is staged in smem).

@@ -63,7 +63,6 @@ SIGNATURES = {
                 P, P, P],
     "cg_split_tf32": [I64, P, P, P, P],
     "cg_split_tf32_t": [INT, P, P, P, P, P, P, I64, P],
-    "cg_pack_bx": [INT, P, P, P, P, P, P, P, I64, P],
     "cg_wgrad_workspace": [I64, INT, INT],
     "cg_wgrad": [I64, INT, INT, P, I64, P, I64, P, P, P, INT, P],
     "cg_colsum": [I64, INT, P, I64, P, P, P],
@@ -129,7 +128,7 @@ KERNEL_ENTRY = {"cg_hash_features", "cg_hash_labels", "cg_scale_rows", "cg_scale
                 "cg_copy_rows", "cg_copy_rows_bounded", "cg_copy_rows_sel",
                 "cg_spmm", "cg_spmm_mb", "cg_relu_bits", "cg_gemm", "cg_gemm_mb", "cg_wgrad",
                 "cg_colsum", "cg_softmax_ce", "cg_adam",
-                "cg_split_tf32", "cg_split_tf32_t", "cg_pack_bx",
+                "cg_split_tf32", "cg_split_tf32_t",
                 "cg_plan_frozen", "cg_set_epoch"}
 launches = {"total": 0}
 

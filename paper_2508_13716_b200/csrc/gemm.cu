@@ -209,8 +209,8 @@ int cg_gemm_mb(int64_t M, int N, int K1, const float *A1, int64_t lda1, const fl
                uint32_t *bits_out, int64_t ld_bits_out, float *C, int64_t ldc, int mode,
                const float *B1_lo, const float *B2_lo, void *stream) {
     if (M == 0 || N == 0) return 0;
-    if (mode != 1 && mode != 2 && mode != 3) {
-        cg_set_error("cg_gemm_mb: mask bits need a tcgen05 mode (1, 2 or 3)");
+    if (mode != 1 && mode != 2) {
+        cg_set_error("cg_gemm_mb: mask bits need a tcgen05 mode (1 or 2)");
         return -1;
     }
     return cg_gemm_tc(M, N, K1, A1, lda1, B1, K2, A2, lda2, B2, trans_b, bias, relu, row_scale,
@@ -230,8 +230,6 @@ int64_t cg_wgrad_workspace(int64_t M, int K, int N) {
 int cg_wgrad(int64_t M, int K, int N, const float *A, int64_t lda, const float *D, int64_t ldd,
              float *dW, float *db, float *ws, int mode, void *stream) {
     if (K == 0 || N == 0) return 0;
-    if (mode == 3) mode = 1;   // activations as B: the bf16 cross-term form needs a packed
-                               // weight operand; weight gradients stay 3xTF32
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t chunk = (mode == 1 || mode == 2) ? wgrad_chunk_tc(M, K, N) : kWgradChunk;
     int64_t nch = (M + chunk - 1) / chunk;

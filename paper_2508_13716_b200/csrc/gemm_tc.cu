@@ -66,10 +66,6 @@ struct Params {
     float *C;
     int64_t ldc;
     int split3;      // 3xTF32
-    int bx;          // mode 3: the two cross terms A_lo B_hi + A B_lo as ONE bf16 MMA of
-                     // doubled K ([A_lo | A] x [B_hi ; B_lo], kind::f16, fp32 accumulate):
-                     // B_lo is the packed bf16 operand (cg_pack_bx), A' = bf16 pairs of
-                     // [A_lo | A] in the A slot's upper 32 TMEM columns
     int b_presplit;  // 3xTF32 with B supplied as (hi, lo) tensors: split A only
     int stages;
     int hi_bytes;    // bytes of [A | B] in one stage (1024-aligned)
@@ -168,12 +164,6 @@ __device__ __forceinline__ uint32_t instr_desc(int a_mn, int b_mn, int N) {
            ((uint32_t)b_mn << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
 
-// kind::f16 instruction descriptor: D f32, A/B bf16, K-major A (TMEM), B major, N, M
-__device__ __forceinline__ uint32_t instr_desc_bf16(int b_mn, int N) {
-    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)b_mn << 16) |
-           ((uint32_t)(N >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-}
-
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
                                          uint32_t acc) {
     asm volatile(
@@ -268,42 +258,6 @@ __device__ __forceinline__ void mma_kblock_ts3(uint32_t d, uint32_t ta, uint64_t
         ::"r"(d), "r"(ta), "l"(db), "l"(dbl), "l"(bstep), "r"(idesc), "r"(acc),
         "r"(smem_u32(bar))
         : "memory");
-}
-
-// bx: 4 kind::tf32 MMAs (A_tf32 [ta, ta+32) x B_hi) + 4 kind::f16 MMAs of K=16
-// (A' [ta+32, ta+64): bf16 pairs of A_lo then A, x B' = bf16 B_hi then B_lo),
-// 8 tensor-core issues instead of 12 for the same 3xTF32-class product
-__device__ __forceinline__ void mma_kblock_bx(uint32_t d, uint32_t ta, uint64_t db, uint64_t dbx,
-                                              uint64_t bstep, uint32_t idt, uint32_t idf,
-                                              uint32_t acc, uint64_t *bar) {
-    asm volatile(
-        "{\n\t.reg .pred e, p;\n\t.reg .b64 b1, b2, b3, x1, x2, x3;\n\t"
-        ".reg .b32 a1, a2, a3, o0, o1, o2, o3;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "setp.ne.b32 p, %7, 0;\n\t"
-        "add.s64 b1, %2, %4; add.s64 b2, b1, %4; add.s64 b3, b2, %4;\n\t"
-        "add.s64 x1, %3, %4; add.s64 x2, x1, %4; add.s64 x3, x2, %4;\n\t"
-        "add.u32 a1, %1, 8; add.u32 a2, %1, 16; add.u32 a3, %1, 24;\n\t"
-        "add.u32 o0, %1, 32; add.u32 o1, %1, 40; add.u32 o2, %1, 48; add.u32 o3, %1, 56;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %5, p;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a1], b1, %5, 1;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a2], b2, %5, 1;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a3], b3, %5, 1;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [o0], %3, %6, 1;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [o1], x1, %6, 1;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [o2], x2, %6, 1;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [o3], x3, %6, 1;\n\t"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%8];\n\t}"
-        ::"r"(d), "r"(ta), "l"(db), "l"(dbx), "l"(bstep), "r"(idt), "r"(idf), "r"(acc),
-        "r"(smem_u32(bar))
-        : "memory");
-}
-
-// bf16 pair (k even in the low half), round to nearest
-__device__ __forceinline__ uint32_t pack_bf16x2(float lo_k, float hi_k) {
-    uint32_t r;
-    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi_k), "f"(lo_k));
-    return r;
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
@@ -499,8 +453,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                             }
                         } else {
                             tma_load_2d(mb, bres_bar, sb, kb * BK, n0);
-                            // bx: the packed bf16 operand has 64 elements per k-block
-                            tma_load_2d(mbl, bres_bar, sbl, kb * BK * (p.bx ? 2 : 1), n0);
+                            tma_load_2d(mbl, bres_bar, sbl, kb * BK, n0);
                         }
                     }
                 }
@@ -583,8 +536,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                         }
                     } else {
                         tma_load_2d(mb, &full[s], sb, k0, tc.n0);
-                        if (p.b_presplit)
-                            tma_load_2d(mbl, &full[s], sb + p.b_lo_off, p.bx ? 2 * k0 : k0, tc.n0);
+                        if (p.b_presplit) tma_load_2d(mbl, &full[s], sb + p.b_lo_off, k0, tc.n0);
                     }
                     }
                     __syncwarp();
@@ -632,16 +584,6 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                                                : sa + A_BYTES;
                     const uint32_t sa_lo = sa + HI_BYTES;
                     const uint32_t sb_lo = sb + (p.bres ? p.bres_lo_off : p.b_lo_off);
-                    if (p.bx) {
-                        // A (TF32) and A' = bf16 [A_lo | A] sit in TMEM slot s
-                        mma_kblock_bx(tmem_d, tmem_base + A_TMEM_COL + 64 * s,
-                                      smem_desc(sb, b_lbo, b_sbo, b_lay),
-                                      smem_desc(sb_lo, b_lbo, b_sbo, b_lay), b_step >> 4, idesc,
-                                      instr_desc_bf16(b_mn, p.BN), first ? 0u : 1u, &empty[s]);
-                        first = false;
-                        __syncwarp();
-                        continue;
-                    }
                     if (p.a_tmem) {
                         // A (= its TF32 truncation) and A_lo sit in TMEM slot s
                         mma_kblock_ts3(tmem_d, tmem_base + A_TMEM_COL + 64 * s,
@@ -1095,20 +1037,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUten
                                                     __uint_as_float(hv[i] & 0xFFFFE000u));
                         const uint32_t ta = tmem_base + ((uint32_t)(32 * q) << 16) + A_TMEM_COL + 64 * s;
                         tmem_st32(ta, hv);
-                        if (p.bx) {
-                            // A' = bf16 pairs of [A_lo | A] (the cross-term operand)
-                            uint32_t pk[32];
-#pragma unroll
-                            for (int i = 0; i < 16; ++i) {
-                                pk[i] = pack_bf16x2(__uint_as_float(lv[2 * i]),
-                                                    __uint_as_float(lv[2 * i + 1]));
-                                pk[16 + i] = pack_bf16x2(__uint_as_float(hv[2 * i]),
-                                                         __uint_as_float(hv[2 * i + 1]));
-                            }
-                            tmem_st32(ta + 32, pk);
-                        } else {
-                            tmem_st32(ta + 32, lv);
-                        }
+                        tmem_st32(ta + 32, lv);
                         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                         mbar_arrive(&conv[s]);
@@ -1217,21 +1146,6 @@ bool make_map(CUtensorMap *m, const float *ptr, int64_t inner, int64_t outer, in
                mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-// The packed bf16 cross-term operand [N x 2 Kp] (cg_pack_bx), box {64, BN}:
-// one 128-byte swizzle row per n and k-block, like a K-major fp32 box {32, BN}.
-bool make_map_bx(CUtensorMap *m, const float *ptr, int64_t K, int64_t N, int box_outer) {
-    encode_fn_t enc = encoder();
-    if (!enc) return false;
-    const int64_t kp2 = 2 * ((K + 31) / 32 * 32);
-    cuuint64_t dims[2] = {(cuuint64_t)kp2, (cuuint64_t)N};
-    cuuint64_t strides[1] = {(cuuint64_t)kp2 * 2};
-    cuuint32_t box[2] = {64u, (cuuint32_t)box_outer};
-    cuuint32_t estr[2] = {1u, 1u};
-    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<float *>(ptr), dims, strides,
-               box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // C viewed as [n_z][M][N] (row stride ldc, z stride M*ldc), box 32 x 32 x 1.
@@ -1422,13 +1336,8 @@ int cg_gemm_tc(int64_t M, int N, int K1, const float *A1, int64_t lda1, const fl
                const uint32_t *mbits, int64_t ld_mbits, uint32_t *bits_out, int64_t ld_bits_out,
                cudaStream_t st) {
     using namespace tc;
-    if (mode != 1 && mode != 2 && mode != 3) {
+    if (mode != 1 && mode != 2) {
         cg_set_error("cg_gemm: unknown mode");
-        return -1;
-    }
-    if (mode == 3 && (!trans_b || !B1_lo || (A2 && K2 > 0 && !B2_lo))) {
-        cg_set_error("cg_gemm: mode 3 needs K-major B (trans_b = 1) with the packed bf16 "
-                     "cross-term operand (cg_pack_bx) as B_lo");
         return -1;
     }
     if ((lda1 % 4) || (A2 && lda2 % 4) || (trans_b ? (K1 % 4) : (N % 4)) ||
@@ -1439,8 +1348,7 @@ int cg_gemm_tc(int64_t M, int N, int K1, const float *A1, int64_t lda1, const fl
     Params p{};
     p.M = M;
     p.N = N;
-    p.split3 = mode == 1 || mode == 3;
-    p.bx = mode == 3;
+    p.split3 = mode == 1;
     p.BN = bn_for(N, p.split3);
     p.bias = bias;
     p.relu = relu;
@@ -1471,9 +1379,7 @@ int cg_gemm_tc(int64_t M, int N, int K1, const float *A1, int64_t lda1, const fl
         bool ok = make_map(&ma[o], As[o], Ks[o], M, ldas[o], BM, false);
         ok = ok && (trans_b ? make_map(&mb[o], Bs[o], Ks[o], N, Ks[o], p.BN, false)
                             : make_map(&mb[o], Bs[o], N, Ks[o], N, 32, true));
-        if (p.bx)
-            ok = ok && make_map_bx(&mbl[o], Bls[o], Ks[o], N, p.BN);
-        else if (p.b_presplit)
+        if (p.b_presplit)
             ok = ok && (trans_b ? make_map(&mbl[o], Bls[o], Ks[o], N, Ks[o], p.BN, false)
                                 : make_map(&mbl[o], Bls[o], N, Ks[o], N, 32, true));
         else

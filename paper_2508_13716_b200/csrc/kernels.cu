@@ -10,7 +10,6 @@
 // All reductions are fixed-order (no float atomics): reruns are bitwise
 // identical.  See DESIGN.md for layouts and rooflines.
 
-#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -720,30 +719,6 @@ __global__ void k_split_tf32_t(const int64_t *__restrict__ off, const int32_t *_
     lo[o + (int64_t)j * r + i] = l;
 }
 
-// The 3xTF32 GEMM's bf16 cross-term operand (mode 3): for a K-major weight
-// split into (hi, lo) [N x K], out [N x 2 Kp] bf16 (Kp = K rounded up to 32)
-// holds per 32-wide k-block kb the 64 values
-//   bf16(hi[n, 32 kb .. 32 kb + 31]) | bf16(lo[n, 32 kb .. 32 kb + 31])
-// (zero past K) -- one 128-byte TMA row per k-block, matching the A' operand
-// [A_lo | A] the GEMM's splitter packs.
-__global__ void k_pack_bx(const int64_t *__restrict__ in_off, const int32_t *__restrict__ nrows,
-                          const int32_t *__restrict__ kcols, const float *__restrict__ hi,
-                          const float *__restrict__ lo, uint16_t *__restrict__ out,
-                          const int64_t *__restrict__ out_off) {
-    pdl_entry();
-    const int m = blockIdx.y;
-    const int N = nrows[m], K = kcols[m];
-    const int Kp2 = 2 * ((K + 31) / 32 * 32);
-    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (e >= (int64_t)N * Kp2) return;
-    const int n = (int)(e / Kp2), q = (int)(e % Kp2);
-    const int kb = q >> 6, j = q & 63;
-    const int k = 32 * kb + (j & 31);
-    float v = 0.f;
-    if (k < K) v = (j < 32 ? hi : lo)[in_off[m] + (int64_t)n * K + k];
-    out[out_off[m] + e] = __bfloat16_as_ushort(__float2bfloat16_rn(v));
-}
-
 __global__ void k_split_tf32(int64_t n, const float *__restrict__ x, float *__restrict__ hi,
                              float *__restrict__ lo) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -1270,17 +1245,6 @@ int cg_split_tf32_t(int n_mats, const int64_t *off, const int32_t *rows, const i
     cgpdl::launch(k_split_tf32_t, grid, dim3(256), 0, (cudaStream_t)stream, off, rows, cols, x,
                   hi, lo);
     CG_CHECK_LAUNCH("k_split_tf32_t");
-    return 1;
-}
-
-int cg_pack_bx(int n_mats, const int64_t *in_off, const int32_t *n_rows, const int32_t *k_cols,
-               const float *hi, const float *lo, uint16_t *out, const int64_t *out_off,
-               int64_t max_elems, void *stream) {
-    if (n_mats == 0 || max_elems == 0) return 0;
-    dim3 grid((unsigned)((max_elems + 255) / 256), (unsigned)n_mats);
-    cgpdl::launch(k_pack_bx, grid, dim3(256), 0, (cudaStream_t)stream, in_off, n_rows, k_cols, hi,
-                  lo, out, out_off);
-    CG_CHECK_LAUNCH("k_pack_bx");
     return 1;
 }
 

@@ -179,37 +179,11 @@ class Engine:
                             _dev([self.pshapes[i][0] for i in mats], torch.int32, dev),
                             _dev([self.pshapes[i][1] for i in mats], torch.int32, dev),
                             len(mats), max(int(np.prod(self.pshapes[i])) for i in mats))
-            # mode 3 (CG_GEMM_BX=1): the forward / input-gradient GEMMs take
-            # their cross terms as one bf16 MMA against packed weights
-            self.use_bx = os.environ.get("CG_GEMM_BX", "0") == "1"
-            if self.use_bx:
-                def kp2(k):
-                    return 2 * ((k + 31) // 32 * 32)
-                offT, off, totT, tot = {}, {}, 0, 0
-                for i in mats:
-                    fi, fo = self.pshapes[i]
-                    offT[i], off[i] = totT, tot
-                    totT += fo * kp2(fi)
-                    tot += fi * kp2(fo)
-                self._bx_offT, self._bx_off = offT, off
-                self.params_bxT = torch.zeros(max(totT, 8), dtype=torch.int16, device=dev)
-                self.params_bx = torch.zeros(max(tot, 8), dtype=torch.int16, device=dev)
-                i64 = torch.int64
-                self._bx_tabs = []
-                for T in (True, False):
-                    rows = [self.pshapes[i][1] if T else self.pshapes[i][0] for i in mats]
-                    cols = [self.pshapes[i][0] if T else self.pshapes[i][1] for i in mats]
-                    outo = [(offT if T else off)[i] for i in mats]
-                    self._bx_tabs.append((
-                        _dev([int(self.poff[i]) for i in mats], i64, dev), _dev(rows, torch.int32, dev),
-                        _dev(cols, torch.int32, dev), _dev(outo, i64, dev), len(mats),
-                        max(r * kp2(c) for r, c in zip(rows, cols)), T))
             call("cg_split_tf32", self.n_params, ptr(self.params), ptr(self.params_hi),
                  ptr(self.params_lo), self.stream())
             self._split_t()
         else:
             self.params_hi = self.params_lo = None
-            self.use_bx = False
         self.grads = torch.zeros(self.n_params + 1, dtype=f32, device=dev)
         self.adam_m = torch.zeros(self.n_params, dtype=f32, device=dev)
         self.adam_v = torch.zeros(self.n_params, dtype=f32, device=dev)
@@ -352,13 +326,6 @@ class Engine:
         off, rows, cols, n, mx = self._wt_tab
         call("cg_split_tf32_t", n, ptr(off), ptr(rows), ptr(cols), ptr(self.params),
              ptr(self.paramsT_hi), ptr(self.paramsT_lo), mx, self.stream())
-        if getattr(self, "use_bx", False):
-            for in_off, rows, cols, out_off, n, mx, T in self._bx_tabs:
-                hi, lo = ((self.paramsT_hi, self.paramsT_lo) if T
-                          else (self.params_hi, self.params_lo))
-                call("cg_pack_bx", n, ptr(in_off), ptr(rows), ptr(cols), ptr(hi), ptr(lo),
-                     ptr(self.params_bxT if T else self.params_bx), ptr(out_off), mx,
-                     self.stream())
 
     def _gemm(self, M, N, K1, A1, lda1, w1, K2=0, A2=None, lda2=0, w2=None, *, trans_b,
               bias=None, relu=0, row_scale=None, mask=None, ldm=0, C, ldc, mask_l=None,
@@ -370,22 +337,13 @@ class Engine:
         mode = self.gemm_mode
         def b(i, arr):
             return None if i is None else ptr(arr) + 4 * int(self.poff[i])
-        def bx(i, T):
-            if i is None:
-                return None
-            return ptr(self.params_bxT if T else self.params_bx) + 2 * (self._bx_offT if T
-                                                                         else self._bx_off)[i]
         if split and trans_b == 0:   # W [K x N] -> its transpose, K-major
             B1, B2 = b(w1, self.paramsT_hi), b(w2, self.paramsT_hi)
             L1, L2 = b(w1, self.paramsT_lo), b(w2, self.paramsT_lo)
-            if self.use_bx:
-                L1, L2, mode = bx(w1, True), bx(w2, True), 3
             trans_b = 1
         elif split:
             B1, B2 = b(w1, self.params_hi), b(w2, self.params_hi)
             L1, L2 = b(w1, self.params_lo), b(w2, self.params_lo)
-            if self.use_bx:
-                L1, L2, mode = bx(w1, False), bx(w2, False), 3
         else:
             B1, B2, L1, L2 = b(w1, self.params), b(w2, self.params), None, None
         mb = self.bits.get(mask_l) if mask_l is not None else None

@@ -402,49 +402,3 @@ def test_spmm_mask_bits_equal_fp32_mask(F, sparse):
              ptr(tb_), F // 32, ptr(b), F, nnz, _st())
         _sync()
         assert torch.equal(a, b)
-
-
-@pytest.mark.parametrize("shape", [(2048, 256, 256, 0), (777, 128, 64, 0), (4099, 48, 40, 0),
-                                   (1000, 64, 96, 40), (169343 // 4, 256, 128, 0)],
-                         ids=lambda s: "x".join(map(str, s)))
-def test_gemm_mode3_bf16_cross_terms(shape):
-    """Mode 3 (3xTF32-class): the cross terms A_lo B_hi + A B_lo as one bf16
-    MMA of doubled K against the packed weight operand (cg_pack_bx); within
-    1e-5 of float64 like mode 1, with bias / ReLU / row scale."""
-    import torch
-    from paper_2508_13716_b200._lib import call, ptr
-    M, N, K1, K2 = shape
-    rng = np.random.default_rng(M + N + K1)
-    A = rng.standard_normal((M, K1)).astype(np.float32)
-    B = rng.standard_normal((N, K1)).astype(np.float32)
-    A2 = rng.standard_normal((M, K2)).astype(np.float32) if K2 else None
-    B2 = rng.standard_normal((N, K2)).astype(np.float32) if K2 else None
-    bias = rng.standard_normal(N).astype(np.float32)
-    rs = rng.random(M).astype(np.float32)
-    ref = A.astype(np.float64) @ B.T.astype(np.float64)
-    if K2:
-        ref += A2.astype(np.float64) @ B2.T.astype(np.float64)
-    ref = np.maximum(ref + bias, 0) * rs[:, None]
-
-    def packed(b):
-        tb = _t(b)
-        h, lo = torch.empty_like(tb), torch.empty_like(tb)
-        call("cg_split_tf32", tb.numel(), ptr(tb), ptr(h), ptr(lo), _st())
-        n, k = b.shape
-        kp2 = 2 * ((k + 31) // 32 * 32)
-        bx = torch.zeros(n * kp2, dtype=torch.int16, device="cuda")
-        z64 = _t(np.zeros(1, np.int64))
-        call("cg_pack_bx", 1, ptr(z64), ptr(_t(np.array([n], np.int32))),
-             ptr(_t(np.array([k], np.int32))), ptr(h), ptr(lo), ptr(bx), ptr(z64), n * kp2, _st())
-        _sync()
-        return h, bx
-    h1, bx1 = packed(B)
-    h2, bx2 = packed(B2) if K2 else (None, None)
-    tA, tA2 = _t(A), (_t(A2) if K2 else None)
-    out = torch.full((M, N), float("nan"), device="cuda")
-    call("cg_gemm", M, N, K1, ptr(tA), K1, ptr(h1), K2, None if tA2 is None else ptr(tA2), K2,
-         None if h2 is None else ptr(h2), 1, ptr(_t(bias)), 1, ptr(_t(rs)), None, 0, ptr(out), N,
-         3, ptr(bx1), None if bx2 is None else ptr(bx2), _st())
-    _sync()
-    err = np.abs(out.cpu().numpy() - ref).max() / np.abs(ref).max()
-    assert err < 1e-5, err
