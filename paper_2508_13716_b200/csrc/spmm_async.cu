@@ -67,7 +67,7 @@ __device__ __forceinline__ void st_out(float4 *p, float4 v, int flags, uint64_t 
 // G lanes per edge stream (a warp runs 32/G independent streams), NCH float4
 // chunks per lane (F <= 4 G NCH), S ring slots per stream, EPI: an addend
 // and/or mask operand is present (its prefetch registers otherwise vanish)
-template <int G, int NCH, int S, bool EPI>
+template <int G, int NCH, int S, int EPI>
 __global__ void __launch_bounds__(WARPS * 32)
 k_spmm_cpa(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
            const int32_t *__restrict__ col, int64_t n_direct, const int32_t *__restrict__ halo_row,
@@ -176,11 +176,11 @@ k_spmm_cpa(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
             // rounds the same way, so they agree bit for bit
             float4 o = make_float4(__fmul_rn(acc[c].x, srow), __fmul_rn(acc[c].y, srow),
                                    __fmul_rn(acc[c].z, srow), __fmul_rn(acc[c].w, srow));
-            if (EPI && addend) {
+            if (EPI == 1 && addend) {
                 o.x = __fadd_rn(o.x, pa[c].x); o.y = __fadd_rn(o.y, pa[c].y);
                 o.z = __fadd_rn(o.z, pa[c].z); o.w = __fadd_rn(o.w, pa[c].w);
             }
-            if (EPI && mask) {
+            if (EPI == 1 && mask) {
                 o.x = pm[c].x > 0.f ? o.x : 0.f; o.y = pm[c].y > 0.f ? o.y : 0.f;
                 o.z = pm[c].z > 0.f ? o.z : 0.f; o.w = pm[c].w > 0.f ? o.w : 0.f;
             }
@@ -228,7 +228,7 @@ k_spmm_cpa(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
     while (row < r_end) close_row();   // trailing rows (incl. edgeless ones)
 }
 
-template <int G, int NCH, int S, bool EPI>
+template <int G, int NCH, int S, int EPI>
 int launch_epi(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col, int64_t n_direct,
            const int32_t *halo_row, const float *X, int64_t ldx, const float *scale,
            const float *addend, int64_t ld_add, const float *mask, int64_t ld_mask,
@@ -264,13 +264,15 @@ int launch(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *col, int
            const float *addend, int64_t ld_add, const float *mask, int64_t ld_mask,
            const uint32_t *mbits, int64_t ld_mbits, float *out,
            int64_t ldo, cudaStream_t st) {
-    return (addend || mask || mbits)
-               ? launch_epi<G, NCH, S, true>(n_rows, F, rowptr, col, n_direct, halo_row, X, ldx,
-                                          scale, addend, ld_add, mask, ld_mask, mbits, ld_mbits, out, ldo,
-                                          st)
-               : launch_epi<G, NCH, S, false>(n_rows, F, rowptr, col, n_direct, halo_row, X, ldx,
-                                           scale, addend, ld_add, mask, ld_mask, mbits, ld_mbits, out, ldo,
-                                          st);
+    // EPI 0: plain; 1: addend and / or fp32 mask (and / or mask bits); 2: mask
+    // bits only -- one register per chunk instead of the fp32 operands' four
+    // or eight, so the GCN backward keeps the forward's lane count
+    const int epi = (addend || mask) ? 1 : (mbits ? 2 : 0);
+#define CG_CPA_EPI(E)                                                                          \
+    launch_epi<G, NCH, S, E>(n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, scale, addend, \
+                             ld_add, mask, ld_mask, mbits, ld_mbits, out, ldo, st)
+    return epi == 1 ? CG_CPA_EPI(1) : epi == 2 ? CG_CPA_EPI(2) : CG_CPA_EPI(0);
+#undef CG_CPA_EPI
 }
 
 }  // namespace cpa
@@ -326,7 +328,7 @@ int cg_spmm_async(int64_t n_rows, int F, const int64_t *rowptr, const int32_t *c
         // 0.088 -> 0.078 ms, 256-wide as two slices 0.197 -> 0.184 ms); the
         // epilogue variant (addend / mask prefetch registers scale with the
         // chunks per lane: 150 registers) stays on 16 lanes (0.21 vs 0.33 ms)
-        const bool epi = addend != nullptr || mask != nullptr || mbits != nullptr;
+        const bool epi = addend != nullptr || mask != nullptr;   // (mask bits alone: 8 lanes)
         if (lanes == 16 || (lanes == 0 && epi)) return launch_s<16, 2, 4, 8>(S, CG_CPA_ARGS);
         if (lanes == 4) return launch_s<4, 8, 3, 4>(S, CG_CPA_ARGS);
         return launch_s<8, 4, 4, 6>(S, CG_CPA_ARGS);
