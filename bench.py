@@ -274,10 +274,19 @@ def run_ours(args):
 
     e2e_run(2, e2e_steps)        # warm-up: copy streams, staging buffer, pinned paths
     torch.cuda.synchronize()
+    # the input buffer's bare H2D rate (no epoch beside it), for the record
+    dbuf = torch.empty_like(host_x, device="cuda")
+    h0 = time.perf_counter()
+    for _ in range(5):
+        dbuf.copy_(host_x, non_blocking=True)
+    torch.cuda.synchronize()
+    h2d_alone = 5 * host_x.numel() * 4 / (time.perf_counter() - h0) / 1e9
+    del dbuf
     barrier()
     torch.cuda.synchronize()
     w0 = time.perf_counter()
     e2e_run(e2e_steps, 0)
+    enq_s = time.perf_counter() - w0      # host time to enqueue the K steps
     torch.cuda.synchronize()
     barrier()
     w_s = time.perf_counter() - w0
@@ -287,6 +296,9 @@ def run_ours(args):
            "h2d_bytes_per_step": int(host_x.numel() * 4),
            "d2h_bytes_per_step": int(D.n_in * eng.C4 * 4 + 4) if args.e2e_logits else 4,
            "steps": e2e_steps, "ms_per_step": w_s / e2e_steps * 1e3,
+           "host_enqueue_ms_per_step": enq_s / e2e_steps * 1e3,
+           "input_h2d_alone_GB_s": h2d_alone,
+           "pcie_bound_ms_per_step": host_x.numel() * 4 / h2d_alone / 1e6,
            "how": "api.TrainSession, 2 untimed warm-up steps, then per step: pinned-host input "
                   "rows H2D (prefetched one step ahead on a copy stream; GCN: row scaling), "
                   "epoch, loss D2H" + (" + logits D2H (overlapping the backward)"

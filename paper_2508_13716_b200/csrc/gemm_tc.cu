@@ -1230,7 +1230,9 @@ int launch(const Params &p0, const CUtensorMap &a0, const CUtensorMap &b0, const
     if (p.a_tmem) {
         p.stage_bytes = A_BYTES + 2 * b_bytes;  // [A | B_hi | B_lo]
         p.b_lo_off = b_bytes;
-        p.acc_stride = 128;
+        // accumulators take the TMEM columns a tile needs (narrow N: 32 / 64),
+        // the A / A_lo slots the rest -- up to 7 slots, a deeper operand ring
+        p.acc_stride = p.BN <= 32 ? 32 : (p.BN <= 64 ? 64 : 128);
     } else {
         p.stage_bytes = p.split3 ? 2 * p.hi_bytes : p.hi_bytes;  // [A | B] [A_lo | B_lo]
         p.b_lo_off = p.hi_bytes;
@@ -1290,7 +1292,9 @@ int launch(const Params &p0, const CUtensorMap &a0, const CUtensorMap &b0, const
     int stages = (SMEM_LIMIT - smem_fixed - p.ring_off) / stage_bytes;
     static const int env_stages = getenv("CG_GEMM_STAGES") ? atoi(getenv("CG_GEMM_STAGES")) : 0;
     int cap = env_stages > 0 ? env_stages : 6;   // experiment knob
-    if (p.a_tmem && cap > 4) cap = 4;            // TMEM: 2 x 128 accumulator + 4 x 64 A columns
+    // TMEM: 2 accumulators + one 64-column A / A_lo slot per stage in 512 columns
+    const int tmem_slots = (512 - 2 * p.acc_stride) / 64;
+    if (p.a_tmem && cap > tmem_slots) cap = tmem_slots;
     p.stages = stages > cap ? cap : stages;
     if (p.stages < 2) {
         cg_set_error("k_gemm_tc: stage does not fit shared memory");
