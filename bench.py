@@ -223,8 +223,7 @@ def run_ours(args):
     # aggregation widths in launch order (backward: min(F_in, F_out) wide;
     # GraphSAGE layer 0 transform-first when it narrows adds a backward one)
     fw, bw = eng.spmm_widths()
-    fb = [spmm_bytes(D.nnz_fwd, D.n_in, F, D.n_halo) for F in fw]
-    bb = [spmm_bytes(D.nnz_bwd, D.n_in, F, 0) for F in bw]
+    fb, bb = eng.spmm_launch_bytes()
     tot_bytes = args.steps * (sum(fb) + sum(bb))
     tot_ms = float(fwd_ms.sum() + bwd_ms.sum())
     achieved = tot_bytes / (tot_ms / 1e3) / 1e9

@@ -254,6 +254,7 @@ class Engine:
             F1 = self.dims[1]
             self.tf0_h = torch.zeros(D.n_in, F1, dtype=f32, device=dev)   # X W_neigh
             self.tf0_p = torch.zeros(D.n_in, F1, dtype=f32, device=dev)   # X W_self + b
+        self._alloc_tfl()
         # backward staging lists
         nb = max(n_bwd, 1)
         self.b_src = _dev(D.bwd_src_dev if n_bwd else [-1], i32, dev)
@@ -299,6 +300,63 @@ class Engine:
         self._io = None
         self.loss_dev = torch.zeros(1, dtype=f32, device=dev)
         torch.cuda.current_stream(self.dev).synchronize()
+
+    def _alloc_tfl(self) -> None:
+        """GCN's last layer transform first when it narrows (C2 256 -> 40,
+        C4 256 -> 47): logits = norm_dst * A (X W) + b aggregates C4-wide rows
+        of H = X_ext W instead of F-wide rows of X_ext.  In the compact layout
+        on one process the layer's sources are fixed -- inner rows and epoch-1
+        snapshot rows -- so the backward has a static transposed CSR over
+        those rows: dH = A^T (norm_dst dL) per source row gives dW = X_ext^T dH,
+        and the input gradient's T = norm_src * (dH[u] + dH[snapshot of u])
+        (the stale-row gradient flows to the owner, DESIGN.md §3 A3).
+        CG_GCN_TFL=0 keeps aggregate-first."""
+        D, L = self.D, self.L
+        l = self.nL - 1
+        # auto: worth it when the edges per transformed row are many -- the
+        # aggregation saves 4 (F - C) bytes per edge, the extra GEMM / dW rows and
+        # the transposed backward cost per row (C4, 13 edges per row: 49.4 ->
+        # 43.1 ms; C2, 4 per row: 1.345 -> 1.354 ms).  CG_GCN_TFL=1 / 0 forces it.
+        env = os.environ.get("CG_GCN_TFL", "")
+        want = env == "1" or (env == "" and D.nnz_fwd >= 8 * max(D.n_rows, 1))
+        self.tfl = (self.kind == "gcn" and self.nL >= 2 and self.dims[self.nL] < self.F[l]
+                    and L.compact and self.comm.world == 1 and D.n_in > 0 and want)
+        if not self.tfl:
+            return
+        dev, i32, i64, f32 = self.dev, torch.int32, torch.int64, torch.float32
+        n_in, C4 = D.n_in, self.dims[self.nL]
+        fcol = np.asarray(D.fwd_col, np.int64)
+        pos = np.maximum(fcol - n_in, 0)
+        src = np.where(fcol < n_in, fcol, np.asarray(D.snap_row_of_pos, np.int64)[pos]
+                       if D.n_halo else fcol)
+        if (src < 0).any():
+            self.tfl = False      # a source without a snapshot row: not the compact plan
+            return
+        dst = np.repeat(np.arange(n_in, dtype=np.int32), np.diff(np.asarray(D.fwd_rowptr)))
+        order = np.argsort(src, kind="stable")     # by source row, then destination
+        rp = np.zeros(D.n_rows + 1, np.int64)
+        np.cumsum(np.bincount(src, minlength=D.n_rows), out=rp[1:])
+        self.tfl_rp, self.tfl_col = _dev(rp, i64, dev), _dev(dst[order], i32, dev)
+        self.tfl_nnz = int(dst.size)
+        # inner row u -> [u, its snapshot row] (the owner receives both gradients)
+        snap_of = np.full(n_in, -1, np.int64)
+        if D.n_snap:
+            mine = np.asarray(D.snap_src_dev) == self.me
+            snap_of[np.asarray(D.snap_src_row)[mine]] = D.snap_off + np.flatnonzero(mine)
+        has = snap_of >= 0
+        urp = np.zeros(n_in + 1, np.int64)
+        np.cumsum(1 + has, out=urp[1:])
+        ucol = np.empty(int(urp[-1]), np.int32)
+        ucol[urp[:-1]] = np.arange(n_in)
+        ucol[urp[:-1][has] + 1] = snap_of[has]
+        self.tfl_urp, self.tfl_ucol = _dev(urp, i64, dev), _dev(ucol, i32, dev)
+        self.tfl_unnz = int(ucol.size)
+        self.tfl_h = torch.zeros(D.n_rows, C4, dtype=f32, device=dev)    # X_ext W
+        self.tfl_dh = torch.zeros(D.n_rows, C4, dtype=f32, device=dev)   # A^T (norm_dst dL)
+        need = max(call("cg_wgrad_workspace", D.n_rows, self.F[l], C4),
+                   (max(D.n_in, D.n_rows) + 255) // 256 * C4)
+        if need > self.ws.numel():
+            self.ws = torch.zeros(need, dtype=f32, device=dev)
 
     def _tabG_ld(self, F: int):
         t = self._tabG_lds.get(F)
@@ -361,12 +419,13 @@ class Engine:
              row_scale, mask, ldm, C, ldc, mode, L1, L2, self.stream())
 
     def _spmm(self, n_rows, F, rowptr, col, n_direct, halo_row, X, ldx, scale, addend, ld_add,
-              mask, ld_mask, out, ldo, mask_l=None):
+              mask, ld_mask, out, ldo, mask_l=None, nnz=None):
         """One cg_spmm call over tensors (the kernel choice and any column
         slicing happen behind the C ABI).  mask_l: the ReLU mask is layer
         mask_l's input (its bits when kept, else the fp32 rows)."""
-        p = lambda t: None if t is None else ptr(t)  # noqa: E731
-        nnz = self.D.nnz_fwd if rowptr is self.fwd_rowptr else self.D.nnz_bwd
+        p = lambda t: None if t is None else (t if isinstance(t, int) else ptr(t))  # noqa: E731
+        if nnz is None:
+            nnz = self.D.nnz_fwd if rowptr is self.fwd_rowptr else self.D.nnz_bwd
         if mask_l is not None:
             mb = self.bits.get(mask_l)
             if mb is not None:
@@ -721,6 +780,9 @@ class Engine:
             if l == 0 and self.tf0:
                 self._forward_tf0(spmm_ev)
                 continue
+            if l == nL - 1 and self.tfl:
+                self._forward_tfl(spmm_ev)
+                continue
             if spmm_ev is not None:
                 self._rec(spmm_ev[l][0])
             hrow = self.halo_row0 if (l == 0 and self.halo_row0 is not None) else self.halo_row
@@ -765,14 +827,68 @@ class Engine:
         call("cg_relu_bits", n_in, Fo, ptr(self.X[1]), Fo, None if b is None else ptr(b),
              0 if b is None else b.shape[1], self.stream())
 
+    def _forward_tfl(self, spmm_ev) -> None:
+        """GCN's last layer, transform first (see _alloc_tfl): H = X_ext W over
+        every row the aggregation reads, then logits = norm_dst * A H + b (the
+        bias as a broadcast addend row)."""
+        l, D = self.nL - 1, self.D
+        F, Fo = self.F[l], self.dims[self.nL]
+        self._gemm(D.n_rows, Fo, F, ptr(self.X[l]), F, 2 * l, trans_b=0, C=ptr(self.tfl_h),
+                   ldc=Fo)
+        if not self._capturing:
+            self._wait_logits_download()
+        if spmm_ev is not None:
+            self._rec(spmm_ev[l][0])
+        self._spmm(D.n_in, Fo, self.fwd_rowptr, self.fwd_col, D.n_in, self.halo_row, self.tfl_h,
+                   Fo, self.norm_dst, self._p(2 * l + 1), 0, None, 0, self.logits, self.C4)
+        if spmm_ev is not None:
+            self._rec(spmm_ev[l][1])
+
+    def _backward_tfl(self, spmm_ev, nxt) -> None:
+        """The last layer's backward under _forward_tfl: dH over the source
+        rows (static transposed CSR, G = norm_dst dL from the loss), dW =
+        X_ext^T dH, db = column sums of dL, T = norm_src * (dH[u] + dH[snap u]),
+        then the masked input gradient mask * (T W^T)."""
+        l, D, st = self.nL - 1, self.D, self.stream()
+        F, Fo = self.F[l], self.dims[self.nL]
+        G = self.Gs[l & 1]
+        if spmm_ev is not None:
+            self._rec(spmm_ev[0][0])
+        self._spmm(D.n_rows, Fo, self.tfl_rp, self.tfl_col, 1 << 62, None, G, Fo, None, None, 0,
+                   None, 0, self.tfl_dh, Fo, nnz=self.tfl_nnz)
+        self._spmm(D.n_in, Fo, self.tfl_urp, self.tfl_ucol, 1 << 62, None, self.tfl_dh, Fo,
+                   self.norm_src, None, 0, None, 0, self.T, Fo, nnz=self.tfl_unnz)
+        if spmm_ev is not None:
+            self._rec(spmm_ev[0][1])
+        call("cg_wgrad", D.n_rows, F, Fo, ptr(self.X[l]), F, ptr(self.tfl_dh), Fo,
+             self._g(2 * l), None, ptr(self.ws), self.wgrad_mode, st)
+        call("cg_colsum", D.n_in, Fo, ptr(self.dL), self.C4, self._g(2 * l + 1), ptr(self.ws), st)
+        self._gemm(D.n_in, F, Fo, ptr(self.T), Fo, 2 * l, trans_b=1, mask_l=l, C=ptr(nxt), ldc=F)
+
     def _n_bwd_spmm(self) -> int:
         return self.nL - 1 + (1 if self.tf0 else 0)
+
+    def spmm_launch_bytes(self):
+        """Algorithmic bytes (DESIGN.md §5 formula) of each timed aggregation
+        window in timer order: (forward per layer, backward windows)."""
+        D = self.D
+
+        def b(nnz, rows, F, halo=0):
+            return nnz * (4 + 4 * F) + rows * (8 + 4 + 4 * F) + 8 + halo * 4
+        fw, bw = self.spmm_widths()
+        fb = [b(D.nnz_fwd, D.n_in, F, D.n_halo) for F in fw]
+        bb = [b(D.nnz_bwd, D.n_in, F) for F in bw]
+        if self.tfl:   # the last layer's window: transposed CSR over X_ext rows + the owner sum
+            bb[0] = (b(self.tfl_nnz, D.n_rows, bw[0]) + b(self.tfl_unnz, D.n_in, bw[0]))
+        return fb, bb
 
     def spmm_widths(self):
         """Row widths of the epoch's aggregations in launch order: (forward
         per layer, backward layers nL-1 .. 1 [, layer 0 under tf0])."""
         w = list(self.F) + [self.C4]
         fwd = [self.dims[1] if (l == 0 and self.tf0) else self.F[l] for l in range(self.nL)]
+        if self.tfl:
+            fwd[-1] = self.dims[self.nL]
         bwd = [min(w[l], w[l + 1]) for l in range(self.nL - 1, 0, -1)]
         if self.tf0:
             bwd.append(self.dims[1])
@@ -808,6 +924,9 @@ class Engine:
         cur = 0
         for l in range(nL - 1, -1, -1):
             F, Fo = self.F[l], self.dims[l + 1]
+            if l == nL - 1 and self.tfl:
+                self._backward_tfl(spmm_ev, self.dY[cur])
+                continue
             dY = self.dL if l == nL - 1 else self.dY[cur]
             # weight gradient(s); the bias gradient (column sums of dY) rides
             # along in the same launch

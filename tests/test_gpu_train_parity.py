@@ -297,3 +297,24 @@ def test_sage_transform_first_layer0_matches_aggregate_first(gemm, monkeypatch):
     for e in range(4):
         assert rel_err(b.logits_per_epoch[e], a.logits_per_epoch[e]) <= FREE_TOL[("sage", gemm)], e
         assert abs(a.losses[e] - b.losses[e]) <= 1e-4 * abs(a.losses[e])
+
+
+@pytest.mark.parametrize("gemm", ["3xtf32", "fp32"])
+def test_gcn_last_layer_transform_first_matches_aggregate_first(gemm, monkeypatch):
+    """GCN's narrowing last layer in both orders (CG_GCN_TFL): logits, loss
+    and the trained weights agree within the parity bound every epoch."""
+    from paper_2508_13716_b200 import hostgraph as H
+    g, ps, og, ops = workload(700, 7.0, 4)
+    f_dim, C = (32, 64, 64), 10
+    caps = make_caps(H, ps, "auto", f_dim)
+    cfg = H.SimConfig(epochs=4, policy="jaca", staleness_bound=-1, f_dim=f_dim, L=3)
+    monkeypatch.setenv("CG_GCN_TFL", "0")
+    a = _train(g, ps, caps, cfg, "gcn", C, gemm=gemm, record_trace=True, keep_params=True)
+    monkeypatch.setenv("CG_GCN_TFL", "1")
+    b = _train(g, ps, caps, cfg, "gcn", C, gemm=gemm, record_trace=True, keep_params=True)
+    assert a.trace_csv == b.trace_csv
+    for e in range(4):
+        assert rel_err(b.logits_per_epoch[e], a.logits_per_epoch[e]) <= TOL, e
+        assert abs(a.losses[e] - b.losses[e]) <= 1e-5 * abs(a.losses[e])
+    for x, y in zip(a.params, b.params):
+        assert rel_err(y, x) <= TOL
