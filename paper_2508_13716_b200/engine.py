@@ -302,24 +302,25 @@ class Engine:
         torch.cuda.current_stream(self.dev).synchronize()
 
     def _alloc_tfl(self) -> None:
-        """GCN's last layer transform first when it narrows (C2 256 -> 40,
-        C4 256 -> 47): logits = norm_dst * A (X W) + b aggregates C4-wide rows
+        """The last layer transform first when it narrows (GCN: C2 256 -> 40,
+        C4 256 -> 47; GraphSAGE: C3 256 -> 41, with X W_self + b as the
+        aggregation's addend): logits = norm_dst * A (X W) + b aggregates C4-wide rows
         of H = X_ext W instead of F-wide rows of X_ext.  In the compact layout
         on one process the layer's sources are fixed -- inner rows and epoch-1
         snapshot rows -- so the backward has a static transposed CSR over
         those rows: dH = A^T (norm_dst dL) per source row gives dW = X_ext^T dH,
         and the input gradient's T = norm_src * (dH[u] + dH[snapshot of u])
         (the stale-row gradient flows to the owner, DESIGN.md §3 A3).
-        CG_GCN_TFL=0 keeps aggregate-first."""
+        CG_TFL=0 keeps aggregate-first."""
         D, L = self.D, self.L
         l = self.nL - 1
         # auto: worth it when the edges per transformed row are many -- the
         # aggregation saves 4 (F - C) bytes per edge, the extra GEMM / dW rows and
         # the transposed backward cost per row (C4, 13 edges per row: 49.4 ->
-        # 43.1 ms; C2, 4 per row: 1.345 -> 1.354 ms).  CG_GCN_TFL=1 / 0 forces it.
-        env = os.environ.get("CG_GCN_TFL", "")
+        # 43.1 ms; C2, 4 per row: 1.345 -> 1.354 ms).  CG_TFL=1 / 0 forces it.
+        env = os.environ.get("CG_TFL", "")
         want = env == "1" or (env == "" and D.nnz_fwd >= 8 * max(D.n_rows, 1))
-        self.tfl = (self.kind == "gcn" and self.nL >= 2 and self.dims[self.nL] < self.F[l]
+        self.tfl = (self.nL >= 2 and self.dims[self.nL] < self.F[l]
                     and L.compact and self.comm.world == 1 and D.n_in > 0 and want)
         if not self.tfl:
             return
@@ -351,8 +352,11 @@ class Engine:
         ucol[urp[:-1][has] + 1] = snap_of[has]
         self.tfl_urp, self.tfl_ucol = _dev(urp, i64, dev), _dev(ucol, i32, dev)
         self.tfl_unnz = int(ucol.size)
-        self.tfl_h = torch.zeros(D.n_rows, C4, dtype=f32, device=dev)    # X_ext W
+        self.tfl_h = torch.zeros(D.n_rows, C4, dtype=f32, device=dev)    # X_ext W (W_neigh)
         self.tfl_dh = torch.zeros(D.n_rows, C4, dtype=f32, device=dev)   # A^T (norm_dst dL)
+        # GraphSAGE: the self term X W_self + b is the aggregation's addend
+        self.tfl_p = (torch.zeros(D.n_in, C4, dtype=f32, device=dev) if self.kind == "sage"
+                      else None)
         need = max(call("cg_wgrad_workspace", D.n_rows, self.F[l], C4),
                    (max(D.n_in, D.n_rows) + 255) // 256 * C4)
         if need > self.ws.numel():
@@ -833,14 +837,20 @@ class Engine:
         bias as a broadcast addend row)."""
         l, D = self.nL - 1, self.D
         F, Fo = self.F[l], self.dims[self.nL]
-        self._gemm(D.n_rows, Fo, F, ptr(self.X[l]), F, 2 * l, trans_b=0, C=ptr(self.tfl_h),
+        sage = self.kind == "sage"
+        w_n = 3 * l + 1 if sage else 2 * l
+        self._gemm(D.n_rows, Fo, F, ptr(self.X[l]), F, w_n, trans_b=0, C=ptr(self.tfl_h),
                    ldc=Fo)
+        if sage:   # GraphSAGE: P = X W_self + b over the inner rows
+            self._gemm(D.n_in, Fo, F, ptr(self.X[l]), F, 3 * l, trans_b=0, bias=self._p(3 * l + 2),
+                       C=ptr(self.tfl_p), ldc=Fo)
         if not self._capturing:
             self._wait_logits_download()
         if spmm_ev is not None:
             self._rec(spmm_ev[l][0])
+        add, ld_add = (self.tfl_p, Fo) if sage else (self._p(2 * l + 1), 0)
         self._spmm(D.n_in, Fo, self.fwd_rowptr, self.fwd_col, D.n_in, self.halo_row, self.tfl_h,
-                   Fo, self.norm_dst, self._p(2 * l + 1), 0, None, 0, self.logits, self.C4)
+                   Fo, self.norm_dst, add, ld_add, None, 0, self.logits, self.C4)
         if spmm_ev is not None:
             self._rec(spmm_ev[l][1])
 
@@ -851,15 +861,27 @@ class Engine:
         then the masked input gradient mask * (T W^T)."""
         l, D, st = self.nL - 1, self.D, self.stream()
         F, Fo = self.F[l], self.dims[self.nL]
+        sage = self.kind == "sage"
         G = self.Gs[l & 1]
         if spmm_ev is not None:
             self._rec(spmm_ev[0][0])
         self._spmm(D.n_rows, Fo, self.tfl_rp, self.tfl_col, 1 << 62, None, G, Fo, None, None, 0,
                    None, 0, self.tfl_dh, Fo, nnz=self.tfl_nnz)
         self._spmm(D.n_in, Fo, self.tfl_urp, self.tfl_ucol, 1 << 62, None, self.tfl_dh, Fo,
-                   self.norm_src, None, 0, None, 0, self.T, Fo, nnz=self.tfl_unnz)
+                   None if sage else self.norm_src, None, 0, None, 0, self.T, Fo,
+                   nnz=self.tfl_unnz)
         if spmm_ev is not None:
             self._rec(spmm_ev[0][1])
+        if sage:
+            # dW_neigh = X_ext^T dH; dW_self (+ db) = X^T dL; the input gradient
+            # mask * (dL W_self^T + T W_neigh^T)
+            call("cg_wgrad", D.n_rows, F, Fo, ptr(self.X[l]), F, ptr(self.tfl_dh), Fo,
+                 self._g(3 * l + 1), None, ptr(self.ws), self.wgrad_mode, st)
+            call("cg_wgrad", D.n_in, F, Fo, ptr(self.X[l]), F, ptr(self.dL), self.C4,
+                 self._g(3 * l), self._g(3 * l + 2), ptr(self.ws), self.wgrad_mode, st)
+            self._gemm(D.n_in, F, Fo, ptr(self.dL), self.C4, 3 * l, Fo, ptr(self.T), Fo, 3 * l + 1,
+                       trans_b=1, mask_l=l, C=ptr(nxt), ldc=F)
+            return
         call("cg_wgrad", D.n_rows, F, Fo, ptr(self.X[l]), F, ptr(self.tfl_dh), Fo,
              self._g(2 * l), None, ptr(self.ws), self.wgrad_mode, st)
         call("cg_colsum", D.n_in, Fo, ptr(self.dL), self.C4, self._g(2 * l + 1), ptr(self.ws), st)

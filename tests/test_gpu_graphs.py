@@ -114,11 +114,12 @@ def test_prefetch_queue_bit_identical(case, graphs, monkeypatch):
         assert np.array_equal(a, b)
 
 
-def test_gcn_last_layer_transform_first_graph_equals_eager(monkeypatch):
+@pytest.mark.parametrize("kind", ["gcn", "sage"])
+def test_last_layer_transform_first_graph_equals_eager(kind, monkeypatch):
     """The transform-first last layer (forced on: the test graph is too sparse
     for the auto rule) replays bit-identically from the epoch graphs."""
-    monkeypatch.setenv("CG_GCN_TFL", "1")
-    case = ("gcn", 600, 6.0, 4, (16, 32, 32), 7, "auto", "jaca", -1, 5, "3xtf32")
+    monkeypatch.setenv("CG_TFL", "1")
+    case = (kind, 600, 6.0, 4, (16, 32, 32), 7, "auto", "jaca", -1, 5, "3xtf32")
     eager, graph = _run(case, False), _run(case, True)
     assert graph.losses == eager.losses
     for a, b in zip(graph.logits_per_epoch, eager.logits_per_epoch):

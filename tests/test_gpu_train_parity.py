@@ -300,21 +300,32 @@ def test_sage_transform_first_layer0_matches_aggregate_first(gemm, monkeypatch):
 
 
 @pytest.mark.parametrize("gemm", ["3xtf32", "fp32"])
-def test_gcn_last_layer_transform_first_matches_aggregate_first(gemm, monkeypatch):
-    """GCN's narrowing last layer in both orders (CG_GCN_TFL): logits, loss
-    and the trained weights agree within the parity bound every epoch."""
+@pytest.mark.parametrize("kind", ["gcn", "sage"])
+def test_last_layer_transform_first_matches_aggregate_first(kind, gemm, monkeypatch):
+    """The narrowing last layer in both orders (CG_TFL; GraphSAGE adds
+    the self term as the aggregation's addend): logits, loss and the trained
+    weights agree within the parity bound every epoch, and the transform-first
+    run matches the oracle."""
     from paper_2508_13716_b200 import hostgraph as H
     g, ps, og, ops = workload(700, 7.0, 4)
     f_dim, C = (32, 64, 64), 10
     caps = make_caps(H, ps, "auto", f_dim)
     cfg = H.SimConfig(epochs=4, policy="jaca", staleness_bound=-1, f_dim=f_dim, L=3)
-    monkeypatch.setenv("CG_GCN_TFL", "0")
-    a = _train(g, ps, caps, cfg, "gcn", C, gemm=gemm, record_trace=True, keep_params=True)
-    monkeypatch.setenv("CG_GCN_TFL", "1")
-    b = _train(g, ps, caps, cfg, "gcn", C, gemm=gemm, record_trace=True, keep_params=True)
+    monkeypatch.setenv("CG_TFL", "0")
+    a = _train(g, ps, caps, cfg, kind, C, gemm=gemm, record_trace=True, keep_params=True)
+    monkeypatch.setenv("CG_TFL", "1")
+    b = _train(g, ps, caps, cfg, kind, C, gemm=gemm, record_trace=True, keep_params=True)
     assert a.trace_csv == b.trace_csv
+    tol = FREE_TOL[(kind, gemm)]
     for e in range(4):
-        assert rel_err(b.logits_per_epoch[e], a.logits_per_epoch[e]) <= TOL, e
+        assert rel_err(b.logits_per_epoch[e], a.logits_per_epoch[e]) <= tol, e
         assert abs(a.losses[e] - b.losses[e]) <= 1e-5 * abs(a.losses[e])
     for x, y in zip(a.params, b.params):
-        assert rel_err(y, x) <= TOL
+        assert rel_err(y, x) <= tol
+    # the transform-first epochs against the oracle run from the GPU's own
+    # weights every epoch (per-epoch arithmetic; free-running drift through
+    # Adam is the stated FREE_TOL matter above, not the order of the layer)
+    _, outs = oracle_run_forced(og, ops, kind, f_dim, C, caps, "jaca", -1, b.params_per_epoch)
+    for e, o in enumerate(outs):
+        assert rel_err(b.logits_per_epoch[e], o.logits) <= 1e-5, e
+        assert abs(b.losses[e] - o.loss) <= 1e-5 * abs(o.loss), e
