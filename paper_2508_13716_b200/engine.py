@@ -18,7 +18,7 @@ import torch
 from . import _lib
 from ._lib import PlanStatic, call, ptr
 from .comm import HostTier, SoloComm
-from .layout import RunLayout
+from .layout import RunLayout, source_row_csrs
 from .planner import EpochPlan, SequentialPlanner
 
 GEMM_MODES = {"fp32": 0, "3xtf32": 1, "tf32": 2}
@@ -326,30 +326,13 @@ class Engine:
             return
         dev, i32, i64, f32 = self.dev, torch.int32, torch.int64, torch.float32
         n_in, C4 = D.n_in, self.dims[self.nL]
-        fcol = np.asarray(D.fwd_col, np.int64)
-        pos = np.maximum(fcol - n_in, 0)
-        src = np.where(fcol < n_in, fcol, np.asarray(D.snap_row_of_pos, np.int64)[pos]
-                       if D.n_halo else fcol)
-        if (src < 0).any():
+        csr = source_row_csrs(D, self.me)
+        if csr is None:
             self.tfl = False      # a source without a snapshot row: not the compact plan
             return
-        dst = np.repeat(np.arange(n_in, dtype=np.int32), np.diff(np.asarray(D.fwd_rowptr)))
-        order = np.argsort(src, kind="stable")     # by source row, then destination
-        rp = np.zeros(D.n_rows + 1, np.int64)
-        np.cumsum(np.bincount(src, minlength=D.n_rows), out=rp[1:])
-        self.tfl_rp, self.tfl_col = _dev(rp, i64, dev), _dev(dst[order], i32, dev)
-        self.tfl_nnz = int(dst.size)
-        # inner row u -> [u, its snapshot row] (the owner receives both gradients)
-        snap_of = np.full(n_in, -1, np.int64)
-        if D.n_snap:
-            mine = np.asarray(D.snap_src_dev) == self.me
-            snap_of[np.asarray(D.snap_src_row)[mine]] = D.snap_off + np.flatnonzero(mine)
-        has = snap_of >= 0
-        urp = np.zeros(n_in + 1, np.int64)
-        np.cumsum(1 + has, out=urp[1:])
-        ucol = np.empty(int(urp[-1]), np.int32)
-        ucol[urp[:-1]] = np.arange(n_in)
-        ucol[urp[:-1][has] + 1] = snap_of[has]
+        rp, col, urp, ucol = csr
+        self.tfl_rp, self.tfl_col = _dev(rp, i64, dev), _dev(col, i32, dev)
+        self.tfl_nnz = int(col.size)
         self.tfl_urp, self.tfl_ucol = _dev(urp, i64, dev), _dev(ucol, i32, dev)
         self.tfl_unnz = int(ucol.size)
         self.tfl_h = torch.zeros(D.n_rows, C4, dtype=f32, device=dev)    # X_ext W (W_neigh)

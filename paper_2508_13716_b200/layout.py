@@ -277,3 +277,42 @@ def build_layout(g, inner, halo, c_gpu, n_dev: int, kind: str,
     layout.owner_dev = part_dev[parts_of[union]].astype(np.int32)
     layout.owner_row = row_of[union].astype(np.int32)
     return layout
+
+
+def source_row_csrs(D, me: int):
+    """The transform-first last layer's two static CSRs (compact layout, one
+    process), for device layout D:
+
+    * by SOURCE row of X_ext (inner row, or the epoch-1 snapshot row a halo
+      position reads): the destination inner rows of its forward edges, in
+      ascending order -- the transpose of the forward CSR after the layer's
+      halo map, so A^T G per source row is one SpMM;
+    * per inner row u: [u, the snapshot row of u] -- the owner sums the
+      gradient of its own row and of its stale copy (A3).
+
+    Returns (rowptr, col, u_rowptr, u_col), or None when some forward source
+    has no snapshot row (not the compact plan)."""
+    n_in = D.n_in
+    fcol = np.asarray(D.fwd_col, np.int64)
+    if D.n_halo:
+        pos = np.maximum(fcol - n_in, 0)
+        src = np.where(fcol < n_in, fcol, np.asarray(D.snap_row_of_pos, np.int64)[pos])
+    else:
+        src = fcol
+    if (src < 0).any():
+        return None
+    dst = np.repeat(np.arange(n_in, dtype=np.int32), np.diff(np.asarray(D.fwd_rowptr)))
+    order = np.argsort(src, kind="stable")     # by source row, then destination
+    rp = np.zeros(D.n_rows + 1, np.int64)
+    np.cumsum(np.bincount(src, minlength=D.n_rows), out=rp[1:])
+    snap_of = np.full(n_in, -1, np.int64)
+    if D.n_snap:
+        mine = np.asarray(D.snap_src_dev) == me
+        snap_of[np.asarray(D.snap_src_row)[mine]] = D.snap_off + np.flatnonzero(mine)
+    has = snap_of >= 0
+    urp = np.zeros(n_in + 1, np.int64)
+    np.cumsum(1 + has, out=urp[1:])
+    ucol = np.empty(int(urp[-1]), np.int32)
+    ucol[urp[:-1]] = np.arange(n_in)
+    ucol[urp[:-1][has] + 1] = snap_of[has]
+    return rp, dst[order], urp, ucol
