@@ -148,8 +148,12 @@ def call(name: str, *args) -> int:
 
 
 def count_replay(per_entry: dict) -> None:
-    """A CUDA-graph replay launches the kernels its capture recorded."""
+    """A CUDA-graph replay launches the kernels its capture recorded
+    (per_entry maps entry point -> kernels; its "total" key, if present, is
+    the same launches summed and is not counted twice)."""
     for name, n in per_entry.items():
+        if name == "total":
+            continue
         launches["total"] += n
         launches[name] = launches.get(name, 0) + n
 
