@@ -15,8 +15,6 @@ from __future__ import annotations
 import csv
 import io
 import json
-import os
-import time
 from dataclasses import dataclass, field
 
 import numpy as np

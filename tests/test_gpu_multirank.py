@@ -22,7 +22,6 @@ import subprocess
 import sys
 import tempfile
 
-import numpy as np
 import pytest
 
 from parity_common import oracle_run, rel_err, workload
