@@ -150,7 +150,12 @@ __device__ __forceinline__ float4 ldg_keep(const float4 *p, uint64_t pol) {
 // inline.  The grid is sized to the resident-block count (persistent), so a
 // group sees many rows and the pipeline stays full.
 template <int G, int NCH>
-__global__ void __launch_bounds__(256)
+// Occupancy matters more than registers for these latency-bound gathers:
+// at 86 registers (the mask-bits and L2-policy operands) the NCH = 2 kernel
+// dropped from 3 to 2 blocks per SM and C3's dense 256-wide aggregation from
+// 8.2 to 10.6 ms; the bound keeps 3 blocks for NCH = 2 (80 registers; the
+// other widths keep the compiler's choice)
+__global__ void __launch_bounds__(256, NCH == 2 ? 3 : 0)
 k_spmm(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
        const int32_t *__restrict__ col, int64_t n_direct, const int32_t *__restrict__ halo_row,
        const float *__restrict__ X, int64_t ldx, const float *__restrict__ scale,
