@@ -153,9 +153,10 @@ template <int G, int NCH>
 // Occupancy matters more than registers for these latency-bound gathers:
 // at 86 registers (the mask-bits and L2-policy operands) the NCH = 2 kernel
 // dropped from 3 to 2 blocks per SM and C3's dense 256-wide aggregation from
-// 8.2 to 10.6 ms; the bound keeps 3 blocks for NCH = 2 (80 registers; the
-// other widths keep the compiler's choice)
-__global__ void __launch_bounds__(256, NCH == 2 ? 3 : 0)
+// 8.2 to 10.6 ms.  Bounded to 4 blocks (64 registers, a few bytes of L1
+// spill) it runs C3's 256-wide aggregations at 7.1-7.4 ms (3 blocks: 8.1-8.4);
+// the other widths keep the compiler's choice
+__global__ void __launch_bounds__(256, NCH == 2 ? 4 : 0)
 k_spmm(int64_t n_rows, int F, const int64_t *__restrict__ rowptr,
        const int32_t *__restrict__ col, int64_t n_direct, const int32_t *__restrict__ halo_row,
        const float *__restrict__ X, int64_t ldx, const float *__restrict__ scale,
